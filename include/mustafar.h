@@ -1,0 +1,179 @@
+/*
+ * mustafar.h -- C ABI of the B200 (sm_100a) Mustafar hot path.
+ *
+ * Mustafar (arXiv 2505.22913) prunes every token's Key and Value head vector to
+ * unstructured sparsity by magnitude, stores the survivors in a bitmap-based sparse
+ * format, and computes decode attention directly on that compressed cache.
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, R# = DESIGN.md "Readings".
+ *
+ * The three calls of the paper's problem statement:
+ *   mstf_prune_compress_kv        "KV cache generated in prefill stage is pruned and
+ *                                  compressed before the start of decode stage"
+ *   mstf_append_token             "KV cache generated in decode stage is kept as-is (dense)
+ *                                  while it is within the local window, then pruned and
+ *                                  compressed afterwards"
+ *   mstf_sparse_decode_attention  Algorithm 1: dense local-window MV + SpMV over
+ *                                  the compressed cache, one softmax over the concatenation.
+ * plus the dense-KV decode baseline mstf_dense_decode_attention (the comparison the
+ * paper's Fig. 5a / Fig. 6 make against dense attention).
+ *
+ * Conventions (all calls):
+ *   - extern "C", no exceptions cross the boundary; every call returns an mstf_status
+ *     (0 = OK, < 0 = error) and validates all host-side arguments BEFORE any launch.
+ *   - Tensor pointers are DEVICE pointers owned by the caller (e.g. allocated by torch);
+ *     the library never allocates or frees device memory and never synchronizes.
+ *     `stream` is a cudaStream_t (passed as void*); work is enqueued on it in order.
+ *   - fp16 means IEEE binary16 bit patterns; all arrays are dense row-major (C order).
+ *   - A "unit" is one (batch, kv-head) pair: U = batch * num_kv_heads, b-major
+ *     (u = b * num_kv_heads + h_kv). G = num_q_heads / num_kv_heads query heads share a
+ *     unit (GQA; query head h_q maps to h_kv = floor(h_q / G), R11), so the query /
+ *     output tensor [batch][num_q_heads][d] is the same memory as [U][G][d].
+ *   - One cache handle per stream (single writer).
+ */
+#ifndef MUSTAFAR_H
+#define MUSTAFAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status codes */
+typedef enum {
+  MSTF_OK = 0,
+  MSTF_EINVAL = -1,     /* null pointer, negative size, bad enum                        */
+  MSTF_ESHAPE = -2,     /* head_dim % 64 != 0, num_q_heads % num_kv_heads != 0, T < 0   */
+  MSTF_EKEEP = -3,      /* keep_k / keep_v outside [1, head_dim]                        */
+  MSTF_ECAPACITY = -4,  /* compressed tokens of some unit would exceed `capacity`       */
+  MSTF_EEMPTY = -5,     /* attention requested while some unit holds 0 tokens           */
+  MSTF_ECUDA = -6,      /* a CUDA launch/runtime error (cudaGetLastError after launch)  */
+  MSTF_ENOTSUP = -7,    /* valid but unsupported here (v1 kernels: head_dim == 128, G<=8)*/
+  MSTF_EWORKSPACE = -8  /* workspace pointer null / too small                          */
+} mstf_status;
+
+/* ------------------------------------------------------------------ configuration */
+typedef struct {
+  int32_t batch;         /* B >= 1                                                        */
+  int32_t num_q_heads;   /* Hq >= 1, multiple of num_kv_heads                             */
+  int32_t num_kv_heads;  /* Hkv >= 1                                                      */
+  int32_t head_dim;      /* d, multiple of 64 (1x64 tiles); kernels: d == 128      */
+  int32_t keep_k;        /* channels kept per Key token, 1..d   (k = d - floor(s*d), R1)  */
+  int32_t keep_v;        /* channels kept per Value token, 1..d (K_s != V_s allowed)*/
+  int32_t window;        /* dense local window W >= 0 (paper: 32)                    */
+  int32_t capacity;      /* max compressed tokens per unit (records per unit)             */
+} mstf_config;
+
+/* k = d - floor(s*d) for s in [0,1) (R1). Returns MSTF_EKEEP for s outside. */
+int32_t mstf_keep_from_sparsity(double sparsity, int32_t head_dim);
+
+/* Packed-value slots per token: ceil(k/8)*8 ("multiples-of-8 padding"; R7). */
+int32_t mstf_k_pad(int32_t keep);
+
+/* ------------------------------------------------------------------ cache buffers
+ * The compressed format ("compressed tiles corresponding to a 1x64 column of the
+ * pruned cache. Per-tile bitmap of 64 bits is used to represent the position of
+ * non-zeros, and tile offset is used to address the correct position of each tile's
+ * starting non-zero"), in the build's per-token record layout (R4-R8):
+ *   token p of unit u, once it has left the window, is record p of that unit;
+ *   BITMAP_x  u64 [U][capacity][d/64]  bit i of word j <=> channel 64j+i kept (LSB first);
+ *                                       exactly keep_x bits set per record (R4)
+ *   VALUES_x  u16 [U][capacity][kpad]   kept fp16 bit patterns in ascending channel order,
+ *                                       then 0x0000 up to kpad = mstf_k_pad(keep_x) (R6, R7)
+ *   OFFSETS_x u32 [U][capacity][d/64]   p*kpad + (kept channels in tiles < j): element index
+ *                                       of tile j's first value in the unit's value array (R8)
+ *   WIN_x     u16 [U][max(W,1)][d]      dense window ring: token p sits in slot p % W (R9)
+ *   N_COMP    i32 [U]                   compressed tokens per unit (device counter)
+ *   N_WIN     i32 [U]                   window tokens per unit, <= W (device counter)
+ * Every buffer must be 16-byte aligned. Contents need no initialisation: prefill writes
+ * the counters. Byte sizes come from mstf_cache_buffer_bytes.                          */
+enum {
+  MSTF_BUF_BITMAP_K = 0, MSTF_BUF_BITMAP_V, MSTF_BUF_VALUES_K, MSTF_BUF_VALUES_V,
+  MSTF_BUF_OFFSETS_K, MSTF_BUF_OFFSETS_V, MSTF_BUF_WIN_K, MSTF_BUF_WIN_V,
+  MSTF_BUF_N_COMP, MSTF_BUF_N_WIN, MSTF_NUM_BUFFERS
+};
+
+/* Host-only. Fills sizes[MSTF_NUM_BUFFERS] (bytes). Validates the config. */
+int mstf_cache_buffer_bytes(const mstf_config* cfg, size_t sizes[MSTF_NUM_BUFFERS]);
+
+/* Opaque HOST handle: a copy of the config, the caller's device pointers and an exact
+ * host mirror of n_comp / n_win (the cache operations are deterministic, so the mirror
+ * lets capacity overflow be detected without a device sync). */
+typedef struct mstf_cache mstf_cache;
+
+/* buffers[i]: device pointer of buffer i (sizes from mstf_cache_buffer_bytes). *out gets
+ * a new handle (host malloc). The handle starts empty (n_comp = n_win = 0 on the mirror;
+ * the device counters are written by the first mstf_prune_compress_kv). */
+int mstf_cache_create(const mstf_config* cfg, void* const buffers[MSTF_NUM_BUFFERS],
+                      mstf_cache** out);
+/* Frees the host handle only (device buffers belong to the caller). NULL is a no-op. */
+int mstf_cache_destroy(mstf_cache* cache);
+/* Host mirror of the per-unit counters (n_comp, n_win may be NULL). No device access. */
+int mstf_cache_counts(const mstf_cache* cache, int32_t* n_comp, int32_t* n_win);
+
+/* ------------------------------------------------------------------ prefill ingest
+ * Resets the cache and ingests a prefill (A10). k, v: fp16 [U][T][d] device.
+ * lengths: optional HOST int32 [U] with 0 <= lengths[u] <= T (ragged prompts; NULL means
+ * every unit holds T tokens). For unit u with L = lengths[u]: tokens 0..L-W-1 are pruned
+ * (per-token magnitude top-keep, lower channel index pruned first on ties: P:62, P:173,
+ * R2, R3) and compressed into records 0..L-W-1; the last min(L, W) tokens are copied
+ * dense into the window ring (R9). Errors: ESHAPE (T < 0), EINVAL (lengths out of range),
+ * ECAPACITY (L - min(L,W) > capacity for some u), ECUDA.                              */
+int mstf_prune_compress_kv(mstf_cache* cache, const void* k, const void* v, int32_t T,
+                           const int32_t* lengths, void* stream);
+
+/* ------------------------------------------------------------------ decode append
+ * Appends one decode token per unit (A11). k_new, v_new: fp16 [U][d] device
+ * (== [batch][num_kv_heads][d]). If a unit's window is full (n_win == W) its oldest window
+ * token (position n_comp) is pruned + compressed into record n_comp and n_comp += 1; the
+ * new token then takes the freed slot. With W == 0 the new token is compressed directly.
+ * Device counters are updated on the device (no host sync; CUDA-graph capturable).
+ * Errors: ECAPACITY (host mirror would exceed capacity), ECUDA.                       */
+int mstf_append_token(mstf_cache* cache, const void* k_new, const void* v_new, void* stream);
+
+/* ------------------------------------------------------------------ decode attention
+ * Algorithm 1 for every unit and each of its G query heads:
+ *   S_C = scale * q K_C^T, S_L = scale * q K_L^T, S = softmax(concat(S_C, S_L)),
+ *   O = S_C V_C + S_L V_L      (K_C, V_C: compressed tokens; K_L, V_L: window tokens).
+ * q: fp16 [U][G][d] device. scale: e.g. 1/sqrt(d) (R10; 1.0 gives the literal Alg. 1).
+ * out: device, [U][G][d] float32 (out_dtype = MSTF_OUT_F32) or fp16 (MSTF_OUT_F16).
+ * workspace: device scratch of >= mstf_workspace_bytes(cache) bytes (split partials).
+ * Split-sequence (flash-decoding) over the compressed tokens; fp16 x fp16 products with
+ * fp32 accumulation; softmax in fp32; the softmax weights enter P.V as fp16.
+ * Errors: EEMPTY (some unit holds no token), EWORKSPACE, ENOTSUP, ECUDA.               */
+enum { MSTF_OUT_F32 = 0, MSTF_OUT_F16 = 1 };
+size_t mstf_workspace_bytes(const mstf_cache* cache);
+int mstf_sparse_decode_attention(const mstf_cache* cache, const void* q, float scale,
+                                 void* out, int32_t out_dtype, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ dense baseline
+ * Dense-KV decode attention with the same kernel skeleton (no pruning): the baseline the
+ * paper compares against (P:439 cuBLAS batched MV, P:458 FlashAttention-2).
+ * k, v: fp16 [U][T_max][d] device; lengths: DEVICE int32 [U] (tokens of each unit, >= 1);
+ * q / out / workspace as above (workspace >= mstf_dense_workspace_bytes).               */
+size_t mstf_dense_workspace_bytes(int32_t units, int32_t group, int32_t head_dim,
+                                  int32_t t_max);
+int mstf_dense_decode_attention(const void* k, const void* v, const int32_t* lengths,
+                                int32_t units, int32_t group, int32_t head_dim,
+                                int32_t t_max, const void* q, float scale, void* out,
+                                int32_t out_dtype, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
+/* ------------------------------------------------------------------ multi-GPU
+ * Contiguous unit range [u0, u1) of rank `rank` among `world`: units are
+ * independent, so a shard is just a cache over its U/world units, and its q / out
+ * slices are contiguous in [B][Hq][d]. Host-only.                                      */
+int mstf_shard_units(int32_t units, int32_t world, int32_t rank, int32_t* u0, int32_t* u1);
+
+/* Human-readable status (static string). */
+const char* mstf_status_string(int32_t status);
+
+/* Library/kernels build identification (static string), e.g. "sm_100a". */
+const char* mstf_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUSTAFAR_H */

@@ -1,0 +1,50 @@
+// kernels.cuh -- launch interfaces shared between the ABI layer (abi.cu) and the
+// kernels (compress.cu, attention.cu). Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mstf {
+
+constexpr int kD = 128;          // head_dim supported by the v1 kernels
+constexpr int kTiles = kD / 64;  // 64-bit bitmap words per token record
+constexpr int kChunk = 64;       // tokens per TMA stage
+constexpr int kConsumerWarps = 4;
+constexpr int kMaxGroup = 8;     // query heads per unit (mma N = 8)
+
+// Device view of one cache (one tensor = K or V shares the same layout).
+struct CacheView {
+  uint64_t* bm[2];      // [U][cap][kTiles]
+  uint16_t* val[2];     // [U][cap][kpad]
+  uint32_t* off[2];     // [U][cap][kTiles]
+  uint16_t* win[2];     // [U][max(W,1)][kD]
+  int32_t* n_comp;      // [U]
+  int32_t* n_win;       // [U]
+  int32_t U, W, cap;
+  int32_t keep[2], kpad[2];
+};
+
+cudaError_t launch_set_counters(const CacheView& c, const int32_t* nc_host, const int32_t* nw_host,
+                                int32_t uniform_T, cudaStream_t s);
+cudaError_t launch_prefill(const CacheView& c, const uint16_t* k, const uint16_t* v, int32_t T,
+                           cudaStream_t s);
+cudaError_t launch_append(const CacheView& c, const uint16_t* k_new, const uint16_t* v_new,
+                          cudaStream_t s);
+
+struct AttnPlan {
+  int32_t splits;        // CTAs per unit along the compressed sequence
+  int32_t nstage;        // TMA ring depth
+  int32_t stage_bytes;   // bytes of one stage (K bm, K vals, V bm, V vals for kChunk tokens)
+};
+AttnPlan plan_attention(int32_t U, int32_t max_comp, int32_t kpad_k, int32_t kpad_v, int32_t sm_count);
+size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits);
+int32_t max_splits_for(int32_t U, int32_t capacity);
+
+cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, int32_t G, const uint16_t* q,
+                                    float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s);
+
+cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const int32_t* lengths, int32_t U,
+                                   int32_t G, int32_t t_max, int32_t splits, const uint16_t* q, float scale,
+                                   void* out, int32_t out_f16, void* ws, cudaStream_t s);
+
+}  // namespace mstf

@@ -1,0 +1,251 @@
+"""Thin Python binding of the C ABI in include/mustafar.h (argument marshalling only).
+
+Every step of the hot path runs in the CUDA kernels of lib/libmustafar.so; this module only
+allocates device buffers with torch, passes pointers/sizes/streams through ctypes and maps
+status codes to exceptions. There is no CPU fallback: if the library or a CUDA device is
+missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libmustafar.so")
+
+# must match include/mustafar.h
+STATUS = {0: "MSTF_OK", -1: "MSTF_EINVAL", -2: "MSTF_ESHAPE", -3: "MSTF_EKEEP", -4: "MSTF_ECAPACITY",
+          -5: "MSTF_EEMPTY", -6: "MSTF_ECUDA", -7: "MSTF_ENOTSUP", -8: "MSTF_EWORKSPACE"}
+BUFFERS = ("bitmap_k", "bitmap_v", "values_k", "values_v", "offsets_k", "offsets_v",
+           "win_k", "win_v", "n_comp", "n_win")
+NUM_BUFFERS = len(BUFFERS)
+OUT_F32, OUT_F16 = 0, 1
+EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "mstf_cache_create",
+           "mstf_cache_destroy", "mstf_cache_counts", "mstf_prune_compress_kv", "mstf_append_token",
+           "mstf_workspace_bytes", "mstf_sparse_decode_attention", "mstf_dense_workspace_bytes",
+           "mstf_dense_decode_attention", "mstf_shard_units", "mstf_status_string", "mstf_build_info")
+
+
+class MustafarError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn}: {STATUS.get(status, status)} ({msg})")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("batch", "num_q_heads", "num_kv_heads", "head_dim", "keep_k", "keep_v", "window", "capacity")]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load lib/libmustafar.so (build it with paper_2505_22913_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2505_22913_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+    sig = {
+        "mstf_keep_from_sparsity": (i32, [ctypes.c_double, i32]),
+        "mstf_k_pad": (i32, [i32]),
+        "mstf_cache_buffer_bytes": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.POINTER(sz)]),
+        "mstf_cache_create": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+        "mstf_cache_destroy": (ctypes.c_int, [vp]),
+        "mstf_cache_counts": (ctypes.c_int, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "mstf_prune_compress_kv": (ctypes.c_int, [vp, vp, vp, i32, ctypes.POINTER(i32), vp]),
+        "mstf_append_token": (ctypes.c_int, [vp, vp, vp, vp]),
+        "mstf_workspace_bytes": (sz, [vp]),
+        "mstf_sparse_decode_attention": (ctypes.c_int, [vp, vp, ctypes.c_float, vp, i32, vp, sz, vp]),
+        "mstf_dense_workspace_bytes": (sz, [i32, i32, i32, i32]),
+        "mstf_dense_decode_attention": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, i32, vp, ctypes.c_float,
+                                                       vp, i32, vp, sz, vp]),
+        "mstf_shard_units": (ctypes.c_int, [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "mstf_status_string": (ctypes.c_char_p, [i32]),
+        "mstf_build_info": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    _lib = L
+    return L
+
+
+def _check(fn: str, st: int):
+    if st != 0:
+        raise MustafarError(fn, st, lib().mstf_status_string(st).decode())
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev_ptr(t: torch.Tensor, dtype=torch.float16, name="tensor") -> int:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the hot path has no CPU fallback)")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor")
+    return t.data_ptr()
+
+
+def keep_from_sparsity(s: float, d: int) -> int:
+    return int(lib().mstf_keep_from_sparsity(float(s), int(d)))
+
+
+def k_pad(keep: int) -> int:
+    return int(lib().mstf_k_pad(int(keep)))
+
+
+def shard_units(units: int, world: int, rank: int):
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _check("mstf_shard_units", lib().mstf_shard_units(units, world, rank, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def buffer_bytes(cfg: Config):
+    sizes = (ctypes.c_size_t * NUM_BUFFERS)()
+    _check("mstf_cache_buffer_bytes", lib().mstf_cache_buffer_bytes(ctypes.byref(cfg), sizes))
+    return [int(x) for x in sizes]
+
+
+@dataclass
+class Shape:
+    batch: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int = 128
+
+    @property
+    def units(self):
+        return self.batch * self.num_kv_heads
+
+    @property
+    def group(self):
+        return self.num_q_heads // self.num_kv_heads
+
+
+class MustafarCache:
+    """One compressed KV cache (one layer, all (batch, kv-head) units) on one device."""
+
+    def __init__(self, batch, num_q_heads, num_kv_heads, head_dim, keep_k, keep_v, window, capacity,
+                 device=None):
+        self.cfg = Config(batch, num_q_heads, num_kv_heads, head_dim, keep_k, keep_v, window, capacity)
+        self.shape = Shape(batch, num_q_heads, num_kv_heads, head_dim)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        sizes = buffer_bytes(self.cfg)
+        # one slab, every buffer 256-byte aligned
+        offs, tot = [], 0
+        for s in sizes:
+            offs.append(tot)
+            tot += (s + 255) // 256 * 256
+        self._slab = torch.empty(max(tot, 256), dtype=torch.uint8, device=self.device)
+        base = self._slab.data_ptr()
+        self._raw = {n: self._slab[o:o + s] for n, o, s in zip(BUFFERS, offs, sizes)}
+        ptrs = (ctypes.c_void_p * NUM_BUFFERS)(*[base + o for o in offs])
+        h = ctypes.c_void_p()
+        _check("mstf_cache_create", lib().mstf_cache_create(ctypes.byref(self.cfg), ptrs, ctypes.byref(h)))
+        self._h = h
+        self._ws = torch.empty(max(int(lib().mstf_workspace_bytes(self._h)), 256), dtype=torch.uint8,
+                               device=self.device)
+        self.keep_k, self.keep_v, self.window, self.capacity = keep_k, keep_v, window, capacity
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.mstf_cache_destroy(h)
+            self._h = None
+
+    @property
+    def units(self):
+        return self.shape.units
+
+    @property
+    def nbytes(self):
+        return self._slab.numel()
+
+    def buffers(self):
+        """Typed views of the device buffers (layout of include/mustafar.h)."""
+        U, cap, d, W = self.units, self.capacity, self.shape.head_dim, max(self.window, 1)
+        nt = d // 64
+        r = self._raw
+        return {
+            "bitmap_k": r["bitmap_k"].view(torch.int64).view(U, cap, nt),
+            "bitmap_v": r["bitmap_v"].view(torch.int64).view(U, cap, nt),
+            "values_k": r["values_k"].view(torch.int16).view(U, cap, k_pad(self.keep_k)),
+            "values_v": r["values_v"].view(torch.int16).view(U, cap, k_pad(self.keep_v)),
+            "offsets_k": r["offsets_k"].view(torch.int32).view(U, cap, nt),
+            "offsets_v": r["offsets_v"].view(torch.int32).view(U, cap, nt),
+            "win_k": r["win_k"].view(torch.int16).view(U, W, d),
+            "win_v": r["win_v"].view(torch.int16).view(U, W, d),
+            "n_comp": r["n_comp"].view(torch.int32),
+            "n_win": r["n_win"].view(torch.int32),
+        }
+
+    def counts(self):
+        U = self.units
+        a, b = (ctypes.c_int32 * U)(), (ctypes.c_int32 * U)()
+        _check("mstf_cache_counts", lib().mstf_cache_counts(self._h, a, b))
+        return list(a), list(b)
+
+    def prune_compress_kv(self, k: torch.Tensor, v: torch.Tensor, lengths=None, stream=None):
+        """k, v: fp16 [U, T, d] (== [B, Hkv, T, d]) on the device."""
+        T = k.shape[-2]
+        ln = None
+        if lengths is not None:
+            ln = (ctypes.c_int32 * self.units)(*[int(x) for x in lengths])
+        _check("mstf_prune_compress_kv",
+               lib().mstf_prune_compress_kv(self._h, _dev_ptr(k, name="k"), _dev_ptr(v, name="v"), T, ln,
+                                            _stream(stream)))
+
+    def append_token(self, k_new: torch.Tensor, v_new: torch.Tensor, stream=None):
+        """k_new, v_new: fp16 [U, d] (== [B, Hkv, d]) on the device."""
+        _check("mstf_append_token", lib().mstf_append_token(self._h, _dev_ptr(k_new, name="k_new"),
+                                                           _dev_ptr(v_new, name="v_new"), _stream(stream)))
+
+    def sparse_decode_attention(self, q: torch.Tensor, scale=None, out=None, out_dtype=torch.float32,
+                                stream=None):
+        """q: fp16 [U, G, d] (== [B, Hq, d]). Returns out [U, G, d] (fp32 or fp16)."""
+        d = self.shape.head_dim
+        scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+        if out is None:
+            out = torch.empty((self.units, self.shape.group, d), dtype=out_dtype, device=self.device)
+        code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
+        _check("mstf_sparse_decode_attention",
+               lib().mstf_sparse_decode_attention(self._h, _dev_ptr(q, name="q"), scale,
+                                                  _dev_ptr(out, out.dtype, "out"), code, self._ws.data_ptr(),
+                                                  self._ws.numel(), _stream(stream)))
+        return out
+
+
+class DenseAttention:
+    """Dense-KV decode attention baseline (same kernel skeleton, no pruning)."""
+
+    def __init__(self, units, group, head_dim, t_max, device=None):
+        self.units, self.group, self.head_dim, self.t_max = units, group, head_dim, t_max
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        n = int(lib().mstf_dense_workspace_bytes(units, group, head_dim, t_max))
+        if n == 0:
+            raise MustafarError("mstf_dense_workspace_bytes", -7, "unsupported shape")
+        self._ws = torch.empty(n, dtype=torch.uint8, device=self.device)
+
+    def __call__(self, k, v, lengths, q, scale=None, out=None, out_dtype=torch.float32, stream=None):
+        scale = 1.0 / math.sqrt(self.head_dim) if scale is None else float(scale)
+        if out is None:
+            out = torch.empty((self.units, self.group, self.head_dim), dtype=out_dtype, device=self.device)
+        code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
+        _check("mstf_dense_decode_attention",
+               lib().mstf_dense_decode_attention(_dev_ptr(k, name="k"), _dev_ptr(v, name="v"),
+                                                 _dev_ptr(lengths, torch.int32, "lengths"), self.units,
+                                                 self.group, self.head_dim, self.t_max, _dev_ptr(q, name="q"),
+                                                 scale, _dev_ptr(out, out.dtype, "out"), code,
+                                                 self._ws.data_ptr(), self._ws.numel(), _stream(stream)))
+        return out

@@ -103,6 +103,20 @@ def fp16_np(shape, seed: int, kind: str = "normal", scale: float = 1.0,
     return _values_from_u64_np(r, kind, scale, chan).reshape(shape)
 
 
+def fp16_np_rows(shape, seed: int, row0: int, nrows: int, kind: str = "normal", scale: float = 1.0,
+                 outlier_channels=(3, 17, 64, 101)) -> np.ndarray:
+    """Rows row0..row0+nrows-1 of fp16_np(shape, ...) viewed as [prod(shape[:-1]), d], without
+    generating the rest (for sampling one unit of a bench-sized tensor on the host)."""
+    d = shape[-1]
+    r = u64_np(nrows * d, seed, start=row0 * d)
+    chan = None
+    if kind == "outlier":
+        ch = np.zeros(d, dtype=bool)
+        ch[[c for c in outlier_channels if c < d]] = True
+        chan = np.tile(ch, nrows)
+    return _values_from_u64_np(r, kind, scale, chan).reshape(nrows, d)
+
+
 # ----------------------------------------------------------------------------- torch
 def _lsr(x, n: int):
     import torch  # noqa: F401

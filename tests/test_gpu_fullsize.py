@@ -1,0 +1,68 @@
+"""Parity at BASELINE.json's full sizes (configs C2-C5) in the launch
+configuration bench.py uses: the whole cache is built and attended on the GPU; the oracle
+recomputes a sample of units one by one (inputs regenerated on the host from the same
+counter-based generator)."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import mustafar_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def M():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_22913_b200 import build as B
+    B.build()
+    from paper_2505_22913_b200 import mustafar
+    return mustafar
+
+
+CASES = {
+    # name: (batch, hq, hkv, T, sparsity_k, sparsity_v, sampled units)
+    "C2_b16_s70": (16, 32, 8, 4096, 0.7, 0.7, (0, 77, 127)),
+    "C2_b1_s50": (1, 32, 8, 4096, 0.5, 0.5, (0, 7)),
+    "C3_mha_32k": (1, 32, 32, 32768, 0.7, 0.7, (0, 31)),
+    "C4_128k_b8": (8, 32, 8, 131072, 0.7, 0.7, (5, 63)),
+    "C5_16k_b64": (64, 32, 8, 16384, 0.7, 0.7, (0, 300, 511)),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fullsize_sampled(M, name):
+    B, hq, hkv, T, sk, sv, sample = CASES[name]
+    U, G, d, W = B * hkv, hq // hkv, 128, 32
+    kk, kv = O.keep_count(sk, d), O.keep_count(sv, d)
+    sK, sV, sQ = (synth.seed_for(7, i) for i in range(3))
+    K = synth.fp16_torch((U, T, d), sK, device="cuda")
+    V = synth.fp16_torch((U, T, d), sV, device="cuda")
+    q = synth.fp16_torch((U, G, d), sQ, device="cuda")
+    gc = M.MustafarCache(B, hq, hkv, d, kk, kv, W, T)
+    gc.prune_compress_kv(K, V)
+    del K, V
+    out = gc.sparse_decode_attention(q, 1 / math.sqrt(d))
+    torch.cuda.synchronize()
+    bufs = gc.buffers()
+    qh = q.cpu().view(torch.int16).numpy().view(np.uint16)
+    for u in sample:
+        Ku = synth.fp16_np_rows((U, T, d), sK, u * T, T).view(np.uint16)
+        Vu = synth.fp16_np_rows((U, T, d), sV, u * T, T).view(np.uint16)
+        oc = O.OracleCache(1, d, kk, kv, W, T)
+        oc.prefill(Ku[None], Vu[None])
+        nc = int(oc.n_comp[0])
+        # format, bit-exact, for the sampled unit
+        assert np.array_equal(bufs["bitmap_k"][u, :nc].cpu().numpy().view(np.uint64), oc.bitmap_k[0, :nc])
+        assert np.array_equal(bufs["values_v"][u, :nc].cpu().numpy().view(np.uint16), oc.values_v[0, :nc])
+        assert np.array_equal(bufs["offsets_k"][u, :nc].cpu().numpy().view(np.uint32), oc.offsets_k[0, :nc])
+        ref = O.attention(oc, qh[u][None], 1 / math.sqrt(d))[0]
+        o = out[u].cpu().numpy().astype(np.float64)
+        err = float((np.abs(o - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max())
+        assert err <= TOL, (name, u, err)
