@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py -- decode-step benchmark of the B200 Mustafar hot path.
+
+A "step" is one decode step of a 32-layer Llama-shaped model's attention over the whole
+batch: for every layer, mstf_append_token (prune + compress the token leaving the dense
+window) followed by mstf_sparse_decode_attention (Algorithm 1), all
+through the C ABI. Synthetic fp16 K/V/Q (seeded counter-based generator, synth/), random
+values of the model's shapes; 32 distinct layer caches (> 3 GB) so the working set is far
+larger than the 126 MB L2 every step.
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload C2] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (weak scaling: batch per rank fixed)
+
+Rank 0 prints ONE JSON line (metric/value/unit/... see the repo contract in DESIGN.md).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-attn µs/step & HBM GB/s at 70% sparsity; tokens/sec vs dense KV"
+LAYERS = 32
+W_WINDOW = 32
+
+# BASELINE.json configs; the bench line runs WORKLOADS[args.workload]
+WORKLOADS = {
+    "C2": dict(desc="Llama-3-8B shape decode, 32 q / 8 kv heads, d=128, 4K context, batch 16, K/V 70% sparsity",
+               batch=16, hq=32, hkv=8, T=4096, sk=0.7, sv=0.7),
+    "C2_s50": dict(desc="Llama-3-8B shape decode, 4K context, batch 16, K/V 50% sparsity",
+                   batch=16, hq=32, hkv=8, T=4096, sk=0.5, sv=0.5),
+    "C3": dict(desc="Llama-2-7B shape MHA decode, 32 heads, d=128, 32K context, batch 1, 70% sparsity",
+               batch=1, hq=32, hkv=32, T=32768, sk=0.7, sv=0.7),
+    "C4": dict(desc="Llama-3-8B shape, 128K context, batch 8, 70% sparsity", batch=8, hq=32, hkv=8, T=131072,
+               sk=0.7, sv=0.7, layers=4),
+    "C5": dict(desc="Llama-3-8B shape, 16K context, batch 64 per GPU, 70% sparsity", batch=64, hq=32, hkv=8,
+               T=16384, sk=0.7, sv=0.7, layers=8),
+}
+
+
+def keep_of(s, d=128):
+    return d - math.floor(s * d)
+
+
+def kpad_of(k):
+    return (k + 7) // 8 * 8
+
+
+def algorithmic_bytes(U, G, n_comp, n_win, keep_k, keep_v, d=128, out_bytes=2):
+    """Bytes one sparse attention call must move: compressed K and V records
+    (bitmaps d/8 B + packed values 2*kpad B each; offsets are not read), the dense window,
+    q and the output. Split partials are an implementation artefact and are not counted."""
+    rec = (d // 8 + 2 * kpad_of(keep_k)) + (d // 8 + 2 * kpad_of(keep_v))
+    return U * (n_comp * rec + n_win * 4 * d + G * d * 2 + G * d * out_bytes)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.dev)], stdout=open(self.path, "w"),
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def oracle_sample(cfg, seconds=10.0, max_units=64):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload: per sampled
+    unit of layer 0, one decode-step append + Alg. 1 attention in float64. Returns
+    (tokens/s extrapolated to the whole workload, description, threads)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    import synth
+    from oracle import mustafar_oracle as O
+    B, hq, hkv, T = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["T"]
+    U, G, d = B * hkv, hq // hkv, 128
+    kk, kv = keep_of(cfg["sk"]), keep_of(cfg["sv"])
+    layers = cfg.get("layers", LAYERS)
+    per_unit = []
+    with threadpool_limits(limits=1):
+        t_budget = time.perf_counter() + seconds
+        for u in range(min(U, max_units)):
+            K = synth.fp16_np_rows((U, T, d), synth.seed_for(2, 0), u * T, T).view(np.uint16)
+            V = synth.fp16_np_rows((U, T, d), synth.seed_for(2, 1), u * T, T).view(np.uint16)
+            oc = O.OracleCache(1, d, kk, kv, W_WINDOW, T + 1)
+            oc.prefill(K[None, :T - 1], V[None, :T - 1])
+            q = synth.fp16_np_rows((U, G, d), synth.seed_for(2, 2), u * G, G).view(np.uint16)
+            t0 = time.perf_counter()
+            oc.append(K[None, T - 1], V[None, T - 1])
+            O.attention(oc, q[None], 1 / math.sqrt(d))
+            per_unit.append(time.perf_counter() - t0)
+            if time.perf_counter() > t_budget:
+                break
+    t_unit = statistics.mean(per_unit)
+    step_s = t_unit * U * layers
+    desc = (f"{len(per_unit)} units of layer 0 (append + fp64 Alg.1 over {T} tokens each), "
+            f"{t_unit * 1e3:.1f} ms/unit, extrapolated x{U} units x{layers} layers")
+    return B / step_s, desc, 1
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, cfg, rank, world, local_rank):
+    import numpy as np  # noqa: F401
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2505_22913_b200 import build as Bld
+    if rank == 0:
+        Bld.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2505_22913_b200 import mustafar as M
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B, hq, hkv, T = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["T"]
+    U, G, d = B * hkv, hq // hkv, 128
+    kk, kv = keep_of(cfg["sk"]), keep_of(cfg["sv"])
+    L = cfg.get("layers", LAYERS) if args.layers is None else args.layers
+    K_steps, W_steps = args.steps, args.warmup
+    total_steps = K_steps + W_steps
+    T0 = T - 1                       # prefill length; the first decode token makes it T
+    cap = T0 - W_WINDOW + 2 * total_steps + 8
+    scale = 1 / math.sqrt(d)
+
+    # ---- caches (one per layer), prefilled from synthetic K/V; dense copies kept for the baseline
+    caches, dense_k, dense_v = [], [], []
+    for l in range(L):
+        seed = synth.seed_for(2, 10 * l + 1000 * rank)
+        Kl = synth.fp16_torch((U, T + total_steps, d), seed, device=dev)
+        Vl = synth.fp16_torch((U, T + total_steps, d), seed + 1, device=dev)
+        c = M.MustafarCache(B, hq, hkv, d, kk, kv, W_WINDOW, cap, device=dev)
+        c.prune_compress_kv(Kl[:, :T0].contiguous(), Vl[:, :T0].contiguous())
+        caches.append(c)
+        if args.dense:
+            dense_k.append(Kl)
+            dense_v.append(Vl)
+        else:
+            del Kl, Vl
+    # per-step decode inputs: q [U,G,d], k_new/v_new [U,d] for every (step, layer), one slab per step
+    per_layer = U * G * d + 2 * U * d
+    gen = synth.fp16_torch((total_steps, L, per_layer), synth.seed_for(2, 7 + rank), device=dev)
+
+    def views(slab, l):
+        x = slab[l]
+        q = x[:U * G * d].view(U, G, d)
+        kn = x[U * G * d:U * G * d + U * d].view(U, d)
+        vn = x[U * G * d + U * d:].view(U, d)
+        return q, kn, vn
+
+    outs = [torch.empty(U, G, d, dtype=torch.float16, device=dev) for _ in range(L)]
+    torch.cuda.synchronize()
+
+    def step(slab, ev=None):
+        for l in range(L):
+            q, kn, vn = views(slab, l)
+            caches[l].append_token(kn, vn)
+            if ev is not None:
+                ev[l][0].record()
+            caches[l].sparse_decode_attention(q, scale, out=outs[l])
+            if ev is not None:
+                ev[l][1].record()
+
+    # ---- device-timed region
+    sampler = ClockSampler(local_rank)
+    attn_ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(L)] for _ in range(K_steps)]
+    for s in range(W_steps):
+        step(gen[s])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in range(K_steps):
+        step(gen[W_steps + s], attn_ev[s])
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / K_steps
+    attn_ms = [attn_ev[s][l][0].elapsed_time(attn_ev[s][l][1]) for s in range(K_steps) for l in range(L)]
+    attn_us = statistics.mean(attn_ms) * 1e3
+    nc, nw = caches[0].counts()
+    n_comp, n_win = nc[0], nw[0]
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the timing
+    host_in = torch.empty((K_steps, L, per_layer), dtype=torch.float16, pin_memory=True)
+    host_in.copy_(gen[W_steps:W_steps + K_steps].cpu())
+    host_out = torch.empty((U, G, d), dtype=torch.float16, pin_memory=True)
+    dev_in = torch.empty((L, per_layer), dtype=torch.float16, device=dev)
+    # re-run the same steps on fresh caches would change n_comp; use the live caches (state moves on)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the caches have capacity for total_steps appends; e2e re-uses the remaining headroom
+    e2e_steps = min(K_steps, cap - (n_comp + 1))
+    e2e_steps = max(1, min(e2e_steps, 8))
+    f0.record()
+    for s in range(e2e_steps):
+        dev_in.copy_(host_in[s], non_blocking=True)
+        step(dev_in)
+        host_out.copy_(outs[L - 1], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+
+    # ---- dense-KV baselines (same shapes, dense fp16 KV of all L layers)
+    dense = {}
+    if args.dense:
+        lengths = torch.full((U,), n_comp + n_win, dtype=torch.int32, device=dev)
+        Tn = n_comp + n_win
+        da = M.DenseAttention(U, G, d, T + total_steps, device=dev)
+        q0 = views(gen[0], 0)[0]
+        o32 = torch.empty(U, G, d, dtype=torch.float16, device=dev)
+
+        def time_dense(fn, reps=3):
+            for l in range(L):
+                fn(l)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                for l in range(L):
+                    fn(l)
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) * 1e3 / (reps * L)
+
+        dense["own_kernel_us_per_layer"] = time_dense(
+            lambda l: da(dense_k[l], dense_v[l], lengths, q0, scale, out=o32))
+        try:
+            import torch.nn.functional as F
+            qs = q0.view(B, hq, 1, d)
+
+            def sdpa(l):
+                k4 = dense_k[l].view(B, hkv, T + total_steps, d)[:, :, :Tn]
+                v4 = dense_v[l].view(B, hkv, T + total_steps, d)[:, :, :Tn]
+                return F.scaled_dot_product_attention(qs, k4, v4, scale=scale, enable_gqa=True)
+            dense["torch_sdpa_us_per_layer"] = time_dense(sdpa)
+        except Exception as ex:  # noqa: BLE001
+            dense["torch_sdpa_error"] = str(ex)[:120]
+        best = min(v for k_, v in dense.items() if k_.endswith("_us_per_layer"))
+        dense["best_dense_us_per_layer"] = best
+        dense["dense_bytes_per_layer"] = U * (Tn * 4 * d + 2 * G * d * 2)
+        dense["dense_tok_s_attention_only"] = B / (L * best * 1e-6)
+
+    # ---- reduce over ranks (max time)
+    import torch as _t
+    vals = _t.tensor([ms, attn_us, e2e_ms], dtype=_t.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, attn_us, e2e_ms = vals.tolist()
+
+    bytes_attn = algorithmic_bytes(U, G, n_comp, n_win, kk, kv)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_attn / (attn_us * 1e-6) / 1e9
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(args.workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    tok_s = world * B / (ms * 1e-3)
+    per_step_in = L * per_layer * 2
+    res = {
+        "metric": METRIC,
+        "value": round(tok_s, 2),
+        "unit": "tokens/s (attention-only decode, 32 layers)" if L == 32 else f"tokens/s (attention-only decode, {L} layers)",
+        "n_gpus": world, "steps": K_steps, "warmup": W_steps,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f16 (fp32 accumulate)",
+        "data": "synthetic (seeded splitmix64 -> fp16 ~N(0,1)); no model weights",
+        "config": {"workload": args.workload, "desc": cfg["desc"], "batch_per_gpu": B, "global_batch": B * world,
+                   "num_q_heads": hq, "num_kv_heads": hkv, "head_dim": d, "context": T, "keep_k": kk, "keep_v": kv,
+                   "window": W_WINDOW, "layers": L, "parallelism": f"dp{world} (batch x kv-head units, no collective)",
+                   "l2": f"inputs larger than L2: {L} layer caches x {caches[0].nbytes / 1e6:.0f} MB"},
+        "us_per_layer_step": round(ms * 1e3 / L, 3),
+        "sparse_attention_us_per_layer": round(attn_us, 3),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "mstf_sparse_decode_attention (K2 split attention + K3 combine), CUDA events per call",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
+                     "algorithmic_bytes_per_launch": bytes_attn},
+        "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": per_step_in, "d2h_bytes_per_step": U * G * d * 2,
+                "steps": e2e_steps, "ms_per_step": round(e2e_ms, 4)},
+        "gpu_launches": K_steps * L * 3,
+        "clocks": clocks,
+        "dense_kv": dense,
+    }
+    if dense.get("best_dense_us_per_layer"):
+        res["speedup_vs_best_dense_attention"] = round(dense["best_dense_us_per_layer"] / attn_us, 3)
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        v, desc, cores = oracle_sample(cfg, seconds=args.cpu_seconds)
+        res["cpu_baseline"] = {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                               "sample": desc}
+    return res
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return None
+    per_step = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        v, desc, cores = oracle_sample(cfg, seconds=0.0, max_units=1)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            per_step.append(v)
+    v = statistics.mean(per_step)
+    B = cfg["batch"]
+    ms = B / v * 1e3
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": cfg["desc"]},
+            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": "each step: " + desc},
+            "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=list(WORKLOADS))
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--no-dense", dest="dense", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "at least 3 warm-up steps"
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    cfg = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        res = run_reference(args, cfg, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, cfg, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -86,8 +86,9 @@ int32_t mstf_k_pad(int32_t keep);
  *   WIN_x     u16 [U][max(W,1)][d]      dense window ring: token p sits in slot p % W (R9)
  *   N_COMP    i32 [U]                   compressed tokens per unit (device counter)
  *   N_WIN     i32 [U]                   window tokens per unit, <= W (device counter)
- * Every buffer must be 16-byte aligned. Contents need no initialisation: prefill writes
- * the counters. Byte sizes come from mstf_cache_buffer_bytes.                          */
+ * Every buffer must be 16-byte aligned. Only N_COMP / N_WIN need initialising: to zero
+ * (an empty cache, matching the handle's host mirror) unless the first call on the cache
+ * is mstf_prune_compress_kv, which writes them. Byte sizes: mstf_cache_buffer_bytes.    */
 enum {
   MSTF_BUF_BITMAP_K = 0, MSTF_BUF_BITMAP_V, MSTF_BUF_VALUES_K, MSTF_BUF_VALUES_V,
   MSTF_BUF_OFFSETS_K, MSTF_BUF_OFFSETS_V, MSTF_BUF_WIN_K, MSTF_BUF_WIN_V,

@@ -150,6 +150,8 @@ class MustafarCache:
         self._slab = torch.empty(max(tot, 256), dtype=torch.uint8, device=self.device)
         base = self._slab.data_ptr()
         self._raw = {n: self._slab[o:o + s] for n, o, s in zip(BUFFERS, offs, sizes)}
+        self._raw["n_comp"].zero_()   # an empty cache (the host mirror starts at 0 too)
+        self._raw["n_win"].zero_()
         ptrs = (ctypes.c_void_p * NUM_BUFFERS)(*[base + o for o in offs])
         h = ctypes.c_void_p()
         _check("mstf_cache_create", lib().mstf_cache_create(ctypes.byref(self.cfg), ptrs, ctypes.byref(h)))
