@@ -33,6 +33,7 @@ namespace mstf {
 
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kBarBytes = 128;  // 8 stages x {full, empty} x 8 B
+constexpr int kBarBytesHost = kBarBytes;
 
 struct AttnParams {
   CacheView c;
@@ -43,140 +44,210 @@ struct AttnParams {
   float scale_log2;
   int nstage, stage_bytes;
   int off_kval, off_vbm, off_vval;  // byte offsets inside a stage (kbm at 0)
+  uint32_t off_pairs;               // byte offset of the per-warp pair-array regions
 };
 
-// ---------------------------------------------------------------- expansion helpers
-// 32 channels of one token (bitmap word `w`, `pre` kept channels before it) from the packed
-// values `vals` (shared or global) -> 16 half2 registers, zero at pruned channels.
-__device__ __forceinline__ void expand_word(const uint16_t* __restrict__ vals, uint32_t w, uint32_t pre,
-                                            uint32_t (&e)[16]) {
-  const uint16_t* p = vals + pre;
+// ---------------------------------------------------------------- smem helpers
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// Mask for dibit j of word w (channels 2j, 2j+1 -> halves lo, hi): 0xFFFF where the
+// channel is kept. cp[s] = w << (7 - s) puts bit 8m+s at the sign bit of byte m;
+// prmt's sign-replicate mode turns the two needed sign bits into byte masks.
+template <int J>
+__device__ __forceinline__ uint32_t dibit_mask(const uint32_t (&cp)[8]) {
+  constexpr int m = J / 4, s0 = 2 * (J % 4);
+  constexpr uint32_t lo = 8 | m, hi = 8 | (4 + m);
+  constexpr uint32_t sel = lo | (lo << 4) | (hi << 8) | (hi << 12);
+  return prmt(cp[s0], cp[s0 + 1], sel);
+}
+
+__device__ __forceinline__ void shifted_copies(uint32_t w, uint32_t (&cp)[8]) {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint32_t b0 = (w >> (2 * i)) & 1u, b1 = (w >> (2 * i + 1)) & 1u;
-    const uint32_t lo = b0 ? (uint32_t)p[0] : 0u;
-    p += b0;
-    const uint32_t hi = b1 ? (uint32_t)p[0] : 0u;
-    p += b1;
-    e[i] = lo | (hi << 16);
-  }
+  for (int s = 0; s < 8; ++s) cp[s] = w * (1u << (7 - s));
 }
 
-// 8 channels (bitmap byte `byte`, `pre` kept channels before it) -> 8 halves in out[0..7].
-__device__ __forceinline__ void expand_byte(const uint16_t* __restrict__ vals, uint32_t byte, uint32_t pre,
-                                            uint32_t (&out)[8]) {
-  const uint16_t* p = vals + pre;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t b = (byte >> i) & 1u;
-    out[i] = b ? (uint32_t)p[0] : 0u;
-    p += b;
-  }
-}
-
-__device__ __forceinline__ uint32_t popc_before_word(const uint4& bw, int t) {
-  return (t > 0 ? __popc(bw.x) : 0) + (t > 1 ? __popc(bw.y) : 0) + (t > 2 ? __popc(bw.z) : 0);
-}
-__device__ __forceinline__ uint32_t word_of(const uint4& bw, int t) {
-  return t == 0 ? bw.x : t == 1 ? bw.y : t == 2 ? bw.z : bw.w;
-}
-
-// Compressed block source: 16 tokens of a stage in shared memory.
-struct CompSrc {
-  const uint4* kbm;      // [kChunk] 16-byte bitmap records
-  const uint16_t* kval;  // [kChunk][kpk]
-  const uint4* vbm;
-  const uint16_t* vval;
-  int kpk, kpv, tok0, nvalid;  // tokens tok0..tok0+15 of the stage, first nvalid valid
-
-  __device__ __forceinline__ bool valid(int r) const { return r < nvalid; }
-  __device__ __forceinline__ void load_k(int r, int t, uint32_t (&e)[16]) const {
-    uint4 bw = kbm[tok0 + r];
-    if (!valid(r)) bw = make_uint4(0, 0, 0, 0);
-    expand_word(kval + (tok0 + r) * kpk, word_of(bw, t), popc_before_word(bw, t), e);
-  }
-  // bytes g and g+8 of token r -> lo[8], hi[8]
-  __device__ __forceinline__ void load_v(int r, int g, uint32_t (&lo)[8], uint32_t (&hi)[8]) const {
-    uint4 bw = vbm[tok0 + r];
-    if (!valid(r)) bw = make_uint4(0, 0, 0, 0);
-    const uint16_t* vals = vval + (tok0 + r) * kpv;
-    const int wl = g >> 2, sh = 8 * (g & 3);
-    const uint32_t wlo = wl ? bw.y : bw.x, whi = wl ? bw.w : bw.z;
-    const uint32_t below = (1u << sh) - 1u;
-    const uint32_t pre_lo = (wl ? __popc(bw.x) : 0) + __popc(wlo & below);
-    const uint32_t pre_hi = __popc(bw.x) + __popc(bw.y) + (wl ? __popc(bw.z) : 0) + __popc(whi & below);
-    expand_byte(vals, (wlo >> sh) & 0xFFu, pre_lo, lo);
-    expand_byte(vals, (whi >> sh) & 0xFFu, pre_hi, hi);
-  }
+// Per-block register operands, already expanded (zeros at pruned channels):
+//   k[r][j] : token g (r=0) / g+8 (r=1), channels 32t+2j, 32t+2j+1   (K mma A operand)
+//   v[x][j] : token {2t, 2t+1, 2t+8, 2t+9}[x], channels 16g+2j, 16g+2j+1 (V mma A operand)
+struct BlockRegs {
+  uint32_t k[2][16];
+  uint32_t v[4][8];
 };
 
-// Dense block source: 16 token rows of fp16 [*, kD] in global memory (window / dense KV).
-struct DenseSrc {
-  const uint16_t* k;   // row pointer base; token r at k + row(r) * kD
+// ---------------------------------------------------------------- compressed source
+// Shifted pair array of one token: Y[m] = (h[m-1], h[m]) (h[-1] = 0), m = 0..kpad, in shared
+// memory, so the pair of values a dibit needs is ONE aligned 32-bit load: for dibit j of a
+// word with exclusive token prefix P, Y[P + popc(word & bits<=2j)] holds (value of channel
+// 2j if kept else previous, value of channel 2j+1 if kept); the mask zeroes pruned halves.
+struct CompBlock {
+  const uint8_t* smem;   // dynamic smem base (generic)
+  uint32_t kbm, kval, vbm, vval;  // byte offsets of this stage's arrays
+  uint32_t yk, yv;       // byte offsets of this warp's pair-array regions
+  int kpk, kpv, tok0, nvalid;
+  uint32_t strk, strv;   // pair-array stride per token (bytes)
+};
+
+__device__ __forceinline__ uint32_t ld_s32(const uint8_t* smem, uint32_t off) {
+  return *reinterpret_cast<const uint32_t*>(smem + off);
+}
+
+// Build the warp's 16 pair arrays of one tensor from the raw packed values of the stage.
+template <int NCH>  // chunks of 8 values per token (kpad / 8); 0 = runtime
+__device__ __forceinline__ void build_pairs(uint8_t* smem, uint32_t raw, uint32_t y, int kp_rt, uint32_t stride,
+                                            int tok0, int lane) {
+  const int nch = NCH ? NCH : (kp_rt >> 3);
+  const int kp = 8 * nch;
+#pragma unroll
+  for (int cid = lane; cid < 16 * nch; cid += 32) {
+    const int tau = cid / nch, c = cid - tau * nch;
+    const uint32_t src = raw + (uint32_t)((tok0 + tau) * kp * 2 + 16 * c);
+    const uint4 a = *reinterpret_cast<const uint4*>(smem + src);
+    const uint32_t nxt = (c + 1 < nch) ? ld_s32(smem, src + 16) : 0u;
+    const uint32_t ybase = y + (uint32_t)tau * stride + 12;  // Y[m] at ybase + 4m
+    uint4 lo, hi;
+    lo.x = a.x; lo.y = prmt(a.x, a.y, 0x5432); lo.z = a.y; lo.w = prmt(a.y, a.z, 0x5432);
+    hi.x = a.z; hi.y = prmt(a.z, a.w, 0x5432); hi.z = a.w; hi.w = prmt(a.w, nxt, 0x5432);
+    *reinterpret_cast<uint4*>(smem + ybase + 4 * (8 * c + 1)) = lo;
+    *reinterpret_cast<uint4*>(smem + ybase + 4 * (8 * c + 5)) = hi;
+    if (c == 0) *reinterpret_cast<uint32_t*>(smem + ybase) = a.x << 16;
+  }
+}
+
+// Expand the 16 dibits of word w (token prefix folded into `base`) into out[16].
+__device__ __forceinline__ void gather_word16(const uint8_t* smem, uint32_t w, uint32_t base, uint32_t (&out)[16]) {
+  uint32_t cp[8];
+  shifted_copies(w, cp);
+#define MSTF_G(J)                                                                 \
+  {                                                                               \
+    const uint32_t pc = __popc(w * (1u << (31 - 2 * J)));                         \
+    out[J] = ld_s32(smem, base + 4u * pc) & dibit_mask<J>(cp);                    \
+  }
+  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
+  MSTF_G(8) MSTF_G(9) MSTF_G(10) MSTF_G(11) MSTF_G(12) MSTF_G(13) MSTF_G(14) MSTF_G(15)
+#undef MSTF_G
+}
+// Expand 8 dibits (bits 0..15 of hw) into out[8].
+__device__ __forceinline__ void gather_half8(const uint8_t* smem, uint32_t hw, uint32_t base, uint32_t (&out)[8]) {
+  uint32_t cp[8];
+  shifted_copies(hw, cp);
+#define MSTF_G(J)                                                                 \
+  {                                                                               \
+    const uint32_t pc = __popc(hw * (1u << (31 - 2 * J)));                        \
+    out[J] = ld_s32(smem, base + 4u * pc) & dibit_mask<J>(cp);                    \
+  }
+  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
+#undef MSTF_G
+}
+
+template <int NK, int NV>
+__device__ __forceinline__ void fill_compressed(const CompBlock& cb, uint8_t* smem, BlockRegs& r, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  // pair arrays for K and V of the warp's 16 tokens
+  build_pairs<NK>(smem, cb.kval, cb.yk, cb.kpk, cb.strk, cb.tok0, lane);
+  build_pairs<NV>(smem, cb.vval, cb.yv, cb.kpv, cb.strv, cb.tok0, lane);
+  // bitmap words (K layout: word t of tokens g, g+8)
+  const bool v0 = g < cb.nvalid, v1 = g + 8 < cb.nvalid;
+  const uint32_t kw0 = v0 ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
+  const uint32_t kw1 = v1 ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
+  const uint32_t vw0 = v0 ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
+  const uint32_t vw1 = v1 ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
+  // exclusive prefix (over t) of word popcounts, two tokens packed in 16-bit halves
+  const uint32_t pk = __popc(kw0) | (__popc(kw1) << 16), pv = __popc(vw0) | (__popc(vw1) << 16);
+  uint32_t ik = pk, iv = pv;
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const uint32_t yk = __shfl_up_sync(0xffffffffu, ik, o, 4), yv = __shfl_up_sync(0xffffffffu, iv, o, 4);
+    if (t >= o) { ik += yk; iv += yv; }
+  }
+  const uint32_t ek = ik - pk, ev = iv - pv;
+  __syncwarp();
+  // K operand
+  const uint32_t bk0 = cb.yk + (uint32_t)g * cb.strk + 12 + 4 * (ek & 0xFFFF);
+  const uint32_t bk1 = bk0 + 8 * cb.strk + 4 * ((ek >> 16) - (ek & 0xFFFF));
+  gather_word16(smem, kw0, bk0, r.k[0]);
+  gather_word16(smem, kw1, bk1, r.k[1]);
+  // V operand: word g/2 (half g%2) of tokens 2t, 2t+1, 2t+8, 2t+9, fetched from the K-layout lanes
+  const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
+  const uint32_t w2t = __shfl_sync(0xffffffffu, vw0, sa), w2t8 = __shfl_sync(0xffffffffu, vw1, sa);
+  const uint32_t w2t1 = __shfl_sync(0xffffffffu, vw0, sb), w2t9 = __shfl_sync(0xffffffffu, vw1, sb);
+  const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
+  const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
+  const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
+  const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
+    const uint32_t base = cb.yv + (uint32_t)tk[x] * cb.strv + 12 + 4 * (ps[x] + extra);
+    gather_half8(smem, ws[x] >> hsh, base, r.v[x]);
+  }
+}
+
+// ---------------------------------------------------------------- dense source
+// 16 dense token rows of fp16 [*, kD] in global memory (window ring / dense KV baseline).
+struct DenseBlock {
+  const uint16_t* k;
   const uint16_t* v;
   int row0, nvalid;
   bool ring;           // window ring: slots row0..row0+15 of a W-slot ring whose oldest
   int W, first, nwin;  // token sits in slot `first` and which holds `nwin` tokens
-
-  __device__ __forceinline__ int row(int r) const { return row0 + r; }
   __device__ __forceinline__ bool valid(int r) const {
     const int slot = row0 + r;
     return ring ? (slot < W && ((slot - first + W) % W) < nwin) : r < nvalid;
   }
-  __device__ __forceinline__ void load_k(int r, int t, uint32_t (&e)[16]) const {
-    if (!valid(r)) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) e[i] = 0;
-      return;
-    }
-    const uint4* p = reinterpret_cast<const uint4*>(k + (size_t)row(r) * kD + 32 * t);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint4 x = p[i];
-      e[4 * i] = x.x; e[4 * i + 1] = x.y; e[4 * i + 2] = x.z; e[4 * i + 3] = x.w;
-    }
-  }
-  __device__ __forceinline__ void load_v(int r, int g, uint32_t (&lo)[8], uint32_t (&hi)[8]) const {
-    if (!valid(r)) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) lo[i] = hi[i] = 0;
-      return;
-    }
-    const uint16_t* base = v + (size_t)row(r) * kD;
-    const uint4 a = *reinterpret_cast<const uint4*>(base + 8 * g);
-    const uint4 b = *reinterpret_cast<const uint4*>(base + 64 + 8 * g);
-    const uint32_t aa[4] = {a.x, a.y, a.z, a.w}, bb[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      lo[2 * i] = aa[i] & 0xFFFFu; lo[2 * i + 1] = aa[i] >> 16;
-      hi[2 * i] = bb[i] & 0xFFFFu; hi[2 * i + 1] = bb[i] >> 16;
-    }
-  }
 };
+
+__device__ __forceinline__ void fill_dense(const DenseBlock& db, BlockRegs& r, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const int tok = g + 8 * x;
+    if (db.valid(tok)) {
+      const uint4* p = reinterpret_cast<const uint4*>(db.k + (size_t)(db.row0 + tok) * kD + 32 * t);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 a = p[i];
+        r.k[x][4 * i] = a.x; r.k[x][4 * i + 1] = a.y; r.k[x][4 * i + 2] = a.z; r.k[x][4 * i + 3] = a.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r.k[x][i] = 0;
+    }
+  }
+  const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    if (db.valid(tk[x])) {
+      const uint4* p = reinterpret_cast<const uint4*>(db.v + (size_t)(db.row0 + tk[x]) * kD + 16 * g);
+      const uint4 a = p[0], b = p[1];
+      r.v[x][0] = a.x; r.v[x][1] = a.y; r.v[x][2] = a.z; r.v[x][3] = a.w;
+      r.v[x][4] = b.x; r.v[x][5] = b.y; r.v[x][6] = b.z; r.v[x][7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) r.v[x][i] = 0;
+    }
+  }
+}
 
 // Per-warp online-softmax attention state.
 struct WarpState {
-  float acc[8][4];  // O^T m-tile i: (ch 8g+i | 64+8g+i) x (heads 2t, 2t+1)
+  float acc[2][4][4];  // [channel parity e][m-tile i]: rows ch 16g+2i+e | 16g+8+2i+e, cols heads 2t, 2t+1
   float m0, m1, l0, l1;
-  uint32_t qf[16];  // q of head g, channels 32t..32t+31 (half2 pairs)
+  uint32_t qf[16];     // q of head g, channels 32t..32t+31 (half2 pairs)
 };
 
-// Process one block of 16 tokens from `src`.
-template <class Src>
-__device__ __forceinline__ void process_block(const Src& src, WarpState& st, float scale_log2, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-  // ---- a5: scores S^T[tok][head]
+// a5 + a7 + a8 for one block of 16 tokens (first/last validity via `vg`, `vg8`).
+__device__ __forceinline__ void process_block(const BlockRegs& r, bool vg, bool vg8, WarpState& st,
+                                              float scale_log2) {
+  // ---- a5: scores S^T[tok][head] (rows tokens g, g+8; cols heads 2t, 2t+1)
   float sc[4] = {0.f, 0.f, 0.f, 0.f};
-  {
-    uint32_t eg[16], eg8[16];
-    src.load_k(g, t, eg);
-    src.load_k(g + 8, t, eg8);
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
-      mma16816(sc, eg[2 * s], eg8[2 * s], eg[2 * s + 1], eg8[2 * s + 1], st.qf[2 * s], st.qf[2 * s + 1]);
-  }
+  for (int s = 0; s < 8; ++s)
+    mma16816(sc, r.k[0][2 * s], r.k[1][2 * s], r.k[0][2 * s + 1], r.k[1][2 * s + 1], st.qf[2 * s], st.qf[2 * s + 1]);
   // ---- a7: online softmax (log2 domain)
-  const bool vg = src.valid(g), vg8 = src.valid(g + 8);
   const float x0 = vg ? sc[0] * scale_log2 : -INFINITY;
   const float x1 = vg ? sc[1] * scale_log2 : -INFINITY;
   const float x2 = vg8 ? sc[2] * scale_log2 : -INFINITY;
@@ -196,37 +267,34 @@ __device__ __forceinline__ void process_block(const Src& src, WarpState& st, flo
   st.m1 = mn1;
   if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      st.acc[i][0] *= a0; st.acc[i][1] *= a1; st.acc[i][2] *= a0; st.acc[i][3] *= a1;
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        st.acc[e][i][0] *= a0; st.acc[e][i][1] *= a1; st.acc[e][i][2] *= a0; st.acc[e][i][3] *= a1;
+      }
+  }
+  // ---- P^T: lane (g,t) gets (p[2t][g], p[2t+1][g]) (kappa 0) and tokens 2t+8, 2t+9 (kappa 1)
+  const uint32_t m[2] = {movmatrix_t(pack_half2(p0, p1)), movmatrix_t(pack_half2(p2, p3))};
+  // ---- a8: O^T[ch pair rows][heads] += V-pairs . P, split into even / odd channels
+#pragma unroll
+  for (int kap = 0; kap < 2; ++kap) {
+    const uint32_t be0 = m[kap] & 0xFFFFu, be1 = m[kap] >> 16, bo0 = m[kap] << 16, bo1 = m[kap] & 0xFFFF0000u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t a0r = r.v[2 * kap][i], a1r = r.v[2 * kap][4 + i];
+      const uint32_t a2r = r.v[2 * kap + 1][i], a3r = r.v[2 * kap + 1][4 + i];
+      mma16816(st.acc[0][i], a0r, a1r, a2r, a3r, be0, be1);
+      mma16816(st.acc[1][i], a0r, a1r, a2r, a3r, bo0, bo1);
     }
   }
-  // ---- P^T fragment (B operand of the V mma): head g, tokens 2t,2t+1 / 2t+8,2t+9
-  const uint32_t pb0 = movmatrix_t(pack_half2(p0, p1));
-  const uint32_t pb1 = movmatrix_t(pack_half2(p2, p3));
-  // ---- a8: O^T += V^T P^T
-  uint32_t A[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) A[i][0] = A[i][1] = A[i][2] = A[i][3] = 0;
-  const int toks[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
-#pragma unroll
-  for (int tk = 0; tk < 4; ++tk) {
-    uint32_t lo[8], hi[8];
-    src.load_v(toks[tk], g, lo, hi);
-    const int sh = 16 * (tk & 1), base = (tk >> 1) * 2;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      A[i][base] |= lo[i] << sh;
-      A[i][base + 1] |= hi[i] << sh;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) mma16816(st.acc[i], A[i][0], A[i][1], A[i][2], A[i][3], pb0, pb1);
 }
 
 __device__ __forceinline__ void init_state(WarpState& st, const uint16_t* q_unit, int G, int lane) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) st.acc[i][0] = st.acc[i][1] = st.acc[i][2] = st.acc[i][3] = 0.f;
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) st.acc[e][i][0] = st.acc[e][i][1] = st.acc[e][i][2] = st.acc[e][i][3] = 0.f;
   st.m0 = st.m1 = -INFINITY;
   st.l0 = st.l1 = 0.f;
   if (g < G) {
@@ -252,29 +320,29 @@ __device__ __forceinline__ void store_partial(WarpState& st, float* ws_o, float*
     l0 += __shfl_xor_sync(0xffffffffu, l0, o);
     l1 += __shfl_xor_sync(0xffffffffu, l1, o);
   }
-  const int h0 = 2 * t, h1 = 2 * t + 1;
   float* o = ws_o + pidx * G * kD;
   float* ml = ws_ml + pidx * G * 2;
-  if (h0 < G) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      o[h0 * kD + 8 * g + i] = st.acc[i][0];
-      o[h0 * kD + 64 + 8 * g + i] = st.acc[i][2];
-    }
-    if (g == 0) { ml[2 * h0] = st.m0; ml[2 * h0 + 1] = l0; }
-  }
-  if (h1 < G) {
+  for (int hh = 0; hh < 2; ++hh) {
+    const int h = 2 * t + hh;
+    if (h < G) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      o[h1 * kD + 8 * g + i] = st.acc[i][1];
-      o[h1 * kD + 64 + 8 * g + i] = st.acc[i][3];
+      for (int i = 0; i < 4; ++i) {
+        *reinterpret_cast<float2*>(o + h * kD + 16 * g + 2 * i) = make_float2(st.acc[0][i][hh], st.acc[1][i][hh]);
+        *reinterpret_cast<float2*>(o + h * kD + 16 * g + 8 + 2 * i) =
+            make_float2(st.acc[0][i][2 + hh], st.acc[1][i][2 + hh]);
+      }
+      if (g == 0) {
+        ml[2 * h] = hh ? st.m1 : st.m0;
+        ml[2 * h + 1] = hh ? l1 : l0;
+      }
     }
-    if (g == 0) { ml[2 * h1] = st.m1; ml[2 * h1 + 1] = l1; }
   }
 }
 
 // ---------------------------------------------------------------- K2: sparse attention
-__global__ void __launch_bounds__(kThreads) mstf_attn_kernel(const AttnParams p) {
+template <int NK, int NV>
+__global__ void __launch_bounds__(kThreads, 2) mstf_attn_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
@@ -326,45 +394,60 @@ __global__ void __launch_bounds__(kThreads) mstf_attn_kernel(const AttnParams p)
   // ---------------- consumers
   WarpState st;
   init_state(st, p.q + (size_t)u * p.G * kD, p.G, lane);
+  const int g = lane >> 2;
+  CompBlock cb;
+  cb.smem = smem;
+  cb.kpk = c.kpad[0];
+  cb.kpv = c.kpad[1];
+  cb.strk = 4 * cb.kpk + 16;
+  cb.strv = 4 * cb.kpv + 16;
+  cb.yk = p.off_pairs + (uint32_t)warp * 16 * (cb.strk + cb.strv);
+  cb.yv = cb.yk + 16 * cb.strk;
+  cb.tok0 = 16 * warp;
   for (int i = 0; i < nchunks; ++i) {
     const int sidx = i % p.nstage;
     mbar_wait(&full[sidx], (i / p.nstage) & 1);
-    const uint8_t* sb = stages + (size_t)sidx * p.stage_bytes;
+    const uint32_t sb = kBarBytes + (uint32_t)sidx * p.stage_bytes;
     const int tok0 = (cbeg + i) * kChunk;
     const int nvalid = min(16, n - tok0 - 16 * warp);
     if (nvalid > 0) {
-      CompSrc src;
-      src.kbm = reinterpret_cast<const uint4*>(sb);
-      src.kval = reinterpret_cast<const uint16_t*>(sb + p.off_kval);
-      src.vbm = reinterpret_cast<const uint4*>(sb + p.off_vbm);
-      src.vval = reinterpret_cast<const uint16_t*>(sb + p.off_vval);
-      src.kpk = c.kpad[0];
-      src.kpv = c.kpad[1];
-      src.tok0 = 16 * warp;
-      src.nvalid = nvalid;
-      process_block(src, st, p.scale_log2, lane);
+      cb.kbm = sb;
+      cb.kval = sb + p.off_kval;
+      cb.vbm = sb + p.off_vbm;
+      cb.vval = sb + p.off_vval;
+      cb.nvalid = nvalid;
+      BlockRegs r;
+      fill_compressed<NK, NV>(cb, smem, r, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sidx]);
+      process_block(r, g < nvalid, g + 8 < nvalid, st, p.scale_log2);
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sidx]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[sidx]);
   }
   // dense local window (Alg. 1 lines 1 and 5) on the last split
   if (split == S - 1 && c.W > 0) {
     const int nw = c.n_win[u];
     const int first = n % c.W;  // slot of the oldest window token (position n)
     for (int blk = warp; blk * 16 < c.W; blk += kConsumerWarps) {
-      DenseSrc src;
-      src.k = c.win[0] + (size_t)u * c.W * kD;
-      src.v = c.win[1] + (size_t)u * c.W * kD;
-      src.ring = true;
-      src.row0 = blk * 16;
-      src.nvalid = 0;
-      src.W = c.W;
-      src.first = first;
-      src.nwin = nw;
+      DenseBlock db;
+      db.k = c.win[0] + (size_t)u * c.W * kD;
+      db.v = c.win[1] + (size_t)u * c.W * kD;
+      db.ring = true;
+      db.row0 = blk * 16;
+      db.nvalid = 0;
+      db.W = c.W;
+      db.first = first;
+      db.nwin = nw;
       bool any = false;
 #pragma unroll
-      for (int r = 0; r < 16; ++r) any |= src.valid(r);
-      if (any) process_block(src, st, p.scale_log2, lane);
+      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
+      if (any) {
+        BlockRegs r;
+        fill_dense(db, r, lane);
+        process_block(r, db.valid(g), db.valid(g + 8), st, p.scale_log2);
+      }
     }
   }
   const size_t pidx = ((size_t)u * S + split) * kConsumerWarps + warp;
@@ -409,14 +492,16 @@ __global__ void __launch_bounds__(kConsumerWarps * 32) mstf_dense_attn_kernel(
   WarpState st;
   init_state(st, q + (size_t)u * G * kD, G, lane);
   for (int b = b0 + warp; b < b1; b += kConsumerWarps) {
-    DenseSrc src;
-    src.k = k + (size_t)u * t_max * kD;
-    src.v = v + (size_t)u * t_max * kD;
-    src.ring = false;
-    src.W = src.first = src.nwin = 0;
-    src.row0 = b * 16;
-    src.nvalid = min(16, n - b * 16);
-    process_block(src, st, scale_log2, lane);
+    DenseBlock db;
+    db.k = k + (size_t)u * t_max * kD;
+    db.v = v + (size_t)u * t_max * kD;
+    db.ring = false;
+    db.W = db.first = db.nwin = 0;
+    db.row0 = b * 16;
+    db.nvalid = min(16, n - b * 16);
+    BlockRegs r;
+    fill_dense(db, r, lane);
+    process_block(r, db.valid(lane >> 2), db.valid((lane >> 2) + 8), st, scale_log2);
   }
   store_partial(st, ws_o, ws_ml, ((size_t)u * S + split) * kConsumerWarps + warp, G, lane);
 }
@@ -437,8 +522,10 @@ size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits) {
 AttnPlan plan_attention(int32_t U, int32_t max_comp, int32_t kpad_k, int32_t kpad_v, int32_t sm_count) {
   AttnPlan pl;
   pl.stage_bytes = kChunk * (16 + 2 * kpad_k + 16 + 2 * kpad_v);
-  int ns = (96 * 1024) / pl.stage_bytes;
-  pl.nstage = ns < 2 ? 2 : (ns > 8 ? 8 : ns);
+  pl.pair_bytes = kConsumerWarps * 16 * ((4 * kpad_k + 16) + (4 * kpad_v + 16));
+  // two CTAs per SM when it fits: ~110 KB per CTA for stages + pair arrays
+  int ns = (110 * 1024 - pl.pair_bytes - kBarBytesHost) / pl.stage_bytes;
+  pl.nstage = ns < 2 ? 2 : (ns > 4 ? 4 : ns);
   const int32_t chunks = (max_comp + kChunk - 1) / kChunk;
   int32_t target = 3 * sm_count;
   int32_t s = (target + U - 1) / U;
@@ -460,13 +547,26 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.off_kval = kChunk * 16;
   p.off_vbm = p.off_kval + kChunk * 2 * c.kpad[0];
   p.off_vval = p.off_vbm + kChunk * 16;
+  p.off_pairs = kBarBytes + plan.nstage * plan.stage_bytes;
   const size_t parts = (size_t)c.U * plan.splits * kConsumerWarps;
   p.ws_o = reinterpret_cast<float*>(ws);
   p.ws_ml = p.ws_o + parts * G * kD;
-  const int smem = kBarBytes + plan.nstage * plan.stage_bytes;
-  cudaError_t e = cudaFuncSetAttribute(mstf_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = kBarBytes + plan.nstage * plan.stage_bytes + plan.pair_bytes;
+  void (*kern)(AttnParams) = mstf_attn_kernel<0, 0>;
+  const int nk = c.kpad[0] / 8, nv = c.kpad[1] / 8;
+  if (nk == nv) {
+    switch (nk) {
+      case 2: kern = mstf_attn_kernel<2, 2>; break;
+      case 4: kern = mstf_attn_kernel<4, 4>; break;
+      case 5: kern = mstf_attn_kernel<5, 5>; break;
+      case 8: kern = mstf_attn_kernel<8, 8>; break;
+      case 16: kern = mstf_attn_kernel<16, 16>; break;
+      default: break;
+    }
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  mstf_attn_kernel<<<dim3(plan.splits, c.U), kThreads, smem, s>>>(p);
+  kern<<<dim3(plan.splits, c.U), kThreads, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   mstf_combine_kernel<<<c.U, G * kD, 0, s>>>(p.ws_o, p.ws_ml, plan.splits * kConsumerWarps, G, out, out_f16);

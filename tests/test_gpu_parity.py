@@ -194,7 +194,7 @@ def test_attention_peaked_softmax_and_fp16_out(M):
 
 
 def test_attention_empty_unit_rejected(M):
-    gc, _ = make(M, 1, 1, 2, 10, 39, 39, 32, lengths=[0, 10], seed=3)
+    gc, _ = make(M, 1, 2, 2, 10, 39, 39, 32, lengths=[0, 10], seed=3)
     q = torch.zeros(2, 1, 128, dtype=torch.float16, device="cuda")
     with pytest.raises(M.MustafarError):
         gc.sparse_decode_attention(q)
