@@ -139,7 +139,9 @@ int mstf_append_token(mstf_cache* cache, const void* k_new, const void* v_new, v
  *   O = S_C V_C + S_L V_L      (K_C, V_C: compressed tokens; K_L, V_L: window tokens).
  * q: fp16 [U][G][d] device. scale: e.g. 1/sqrt(d) (R10; 1.0 gives the literal Alg. 1).
  * out: device, [U][G][d] float32 (out_dtype = MSTF_OUT_F32) or fp16 (MSTF_OUT_F16).
- * workspace: device scratch of >= mstf_workspace_bytes(cache) bytes (split partials).
+ * workspace: device scratch of >= mstf_workspace_bytes(cache) bytes (split partials and per-unit
+ *            arrival tickets); it must be zero-filled once before its first use -- every call
+ *            leaves the tickets at zero again. One workspace per concurrently running call.
  * Split-sequence (flash-decoding) over the compressed tokens; fp16 x fp16 products with
  * fp32 accumulation; softmax in fp32; the softmax weights enter P.V as fp16.
  * Errors: EEMPTY (some unit holds no token), EWORKSPACE, ENOTSUP, ECUDA.               */

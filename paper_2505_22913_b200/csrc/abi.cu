@@ -172,6 +172,10 @@ int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale
   }
   const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
   AttnPlan plan = plan_attention(h->view.U, max_comp, h->view.kpad[0], h->view.kpad[1], sm_count());
+  if (const char* env = std::getenv("MSTF_SPLITS")) {  // tuning override (not part of the ABI contract)
+    const int v = std::atoi(env);
+    if (v > 0) plan.splits = v;
+  }
   if (plan.splits > h->max_splits) plan.splits = h->max_splits;
   if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, out,
                               out_dtype == MSTF_OUT_F16, ws, static_cast<cudaStream_t>(stream)) != cudaSuccess)

@@ -25,6 +25,7 @@
 //     g+8 of tokens 2t, 2t+1, 2t+8, 2t+9.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -45,6 +46,11 @@ struct AttnParams {
   int nstage, stage_bytes;
   int off_kval, off_vbm, off_vval;  // byte offsets inside a stage (kbm at 0)
   uint32_t off_pairs;               // byte offset of the per-warp pair-array regions
+  uint32_t off_handoff;             // byte offset of the K->V mailbox (split kernel)
+  uint32_t reg_k, reg_v;            // per-warp pair-array region bytes (K, V)
+  int* tickets;                     // [U] arrival counters for the fused combine
+  void* out;
+  int out_f16;
 };
 
 // ---------------------------------------------------------------- smem helpers
@@ -186,6 +192,203 @@ __device__ __forceinline__ void fill_compressed(const CompBlock& cb, uint8_t* sm
   }
 }
 
+// K half: pair arrays of the 16 K tokens, then the K operand (k[2][16]).
+template <int NK>
+__device__ __forceinline__ void fill_k(const CompBlock& cb, uint8_t* smem, uint32_t (&kr)[2][16], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  build_pairs<NK>(smem, cb.kval, cb.yk, cb.kpk, cb.strk, cb.tok0, lane);
+  const uint32_t kw0 = g < cb.nvalid ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
+  const uint32_t kw1 = g + 8 < cb.nvalid ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
+  const uint32_t pk = __popc(kw0) | (__popc(kw1) << 16);
+  uint32_t ik = pk;
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
+    if (t >= o) ik += y;
+  }
+  const uint32_t ek = ik - pk;
+  __syncwarp();
+  const uint32_t bk0 = cb.yk + (uint32_t)g * cb.strk + 12 + 4 * (ek & 0xFFFF);
+  const uint32_t bk1 = bk0 + 8 * cb.strk + 4 * ((ek >> 16) - (ek & 0xFFFF));
+  gather_word16(smem, kw0, bk0, kr[0]);
+  gather_word16(smem, kw1, bk1, kr[1]);
+}
+
+// V half: pair arrays of the 16 V tokens, then the V operand (v[4][8]).
+template <int NV>
+__device__ __forceinline__ void fill_v(const CompBlock& cb, uint8_t* smem, uint32_t (&vr)[4][8], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  build_pairs<NV>(smem, cb.vval, cb.yv, cb.kpv, cb.strv, cb.tok0, lane);
+  const uint32_t vw0 = g < cb.nvalid ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
+  const uint32_t vw1 = g + 8 < cb.nvalid ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
+  const uint32_t pv = __popc(vw0) | (__popc(vw1) << 16);
+  uint32_t iv = pv;
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o, 4);
+    if (t >= o) iv += y;
+  }
+  const uint32_t ev = iv - pv;
+  __syncwarp();
+  const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
+  const uint32_t w2t = __shfl_sync(0xffffffffu, vw0, sa), w2t8 = __shfl_sync(0xffffffffu, vw1, sa);
+  const uint32_t w2t1 = __shfl_sync(0xffffffffu, vw0, sb), w2t9 = __shfl_sync(0xffffffffu, vw1, sb);
+  const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
+  const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
+  const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
+  const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
+    const uint32_t base = cb.yv + (uint32_t)tk[x] * cb.strv + 12 + 4 * (ps[x] + extra);
+    gather_half8(smem, ws[x] >> hsh, base, vr[x]);
+  }
+}
+
+// ---------------------------------------------------------------- interleaved pair arrays (v3)
+// Thread-per-token build: lane L handles token tau = L >> 1, half h = L & 1 of one tensor's 16
+// tokens. With kp = kpad, half h writes entries m = M0(h) + e, e = 0..E-1, E = kp/2 + 2,
+// M0(1) = kp/2 + 2 (entries past kp are padding rows). Y[m] = (h[m-1], h[m]).
+// Layouts (word offsets inside a warp region; 32-bit entries):
+//   K : region K_{tau>>3}, word 8*m + (tau & 7)        -> a K gather row touches 8 tokens in
+//       distinct banks; regions K0/K1 sit 8 banks apart so the build stores are conflict-free
+//   V : region V_r, r = (tau & 1) + 2*(tau >> 3), word 4*m + ((tau >> 1) & 3)
+//       -> a V gather touches 4 tokens x 8 lanes; region bank offsets {0, 4, 16, 20}.
+template <int NCH>
+struct PairGeom {
+  static constexpr int kp = 8 * NCH;
+  static constexpr int E = kp / 2 + 2;   // entries per half-lane
+  static constexpr int rows = kp + 4;    // rows per region (>= M0(1) + E)
+  static constexpr int nw = E / 2 + 1;   // raw words loaded per half-lane
+};
+
+// Region word offsets, padded so that region bases have the required bank offsets.
+__host__ __device__ constexpr int pad_to_bank(int off, int bank) {
+  return off + ((bank - (off & 31)) & 31);
+}
+template <int NCH>
+struct KLayout {
+  static constexpr int rows = PairGeom<NCH>::rows;
+  static constexpr int k0 = 0;
+  static constexpr int k1 = pad_to_bank(k0 + 8 * rows, 8);
+  static constexpr int words = k1 + 8 * rows;
+};
+template <int NCH>
+struct VLayout {
+  static constexpr int rows = PairGeom<NCH>::rows;
+  static constexpr int v0 = 0;
+  static constexpr int v1 = pad_to_bank(v0 + 4 * rows, 4);
+  static constexpr int v2 = pad_to_bank(v1 + 4 * rows, 16);
+  static constexpr int v3 = pad_to_bank(v2 + 4 * rows, 20);
+  static constexpr int words = v3 + 4 * rows;
+  __host__ __device__ static constexpr int region(int r) { return r == 0 ? v0 : r == 1 ? v1 : r == 2 ? v2 : v3; }
+};
+
+template <int NCH, bool IS_V>
+__device__ __forceinline__ void build_interleaved(uint8_t* smem, uint32_t raw, uint32_t ybase, int tok0, int lane) {
+  using Gm = PairGeom<NCH>;
+  const int tau = lane >> 1, h = lane & 1;
+  const int m0 = h ? Gm::kp / 2 + 2 : 0;
+  // raw words wb .. wb + nw - 1 of token tau, wb = m0/2 - 1 (word -1 == 0)
+  const uint32_t src = raw + (uint32_t)((tok0 + tau) * Gm::kp * 2) + 4u * (uint32_t)(m0 / 2 - 1);
+  uint32_t W[Gm::nw];
+  W[0] = h ? ld_s32(smem, src) : 0u;
+#pragma unroll
+  for (int i = 1; i < Gm::nw; ++i) W[i] = ld_s32(smem, src + 4 * i);
+  uint32_t dst, step;
+  if (IS_V) {
+    const int r = (tau & 1) + 2 * (tau >> 3);
+    dst = ybase + 4u * (uint32_t)(VLayout<NCH>::region(r) + ((tau >> 1) & 3) + 4 * m0);
+    step = 16;
+  } else {
+    dst = ybase + 4u * (uint32_t)((tau >> 3 ? KLayout<NCH>::k1 : KLayout<NCH>::k0) + (tau & 7) + 8 * m0);
+    step = 32;
+  }
+#pragma unroll
+  for (int e = 0; e < Gm::E; ++e) {
+    const uint32_t y = (e & 1) ? W[(e + 1) >> 1] : prmt(W[e >> 1], W[(e >> 1) + 1], 0x5432);
+    *reinterpret_cast<uint32_t*>(smem + dst + step * e) = y;
+  }
+}
+
+// Expand 16 dibits of word w; entry r of this token's pair array at base + stride * r.
+template <int STRIDE>
+__device__ __forceinline__ void gather16_s(const uint8_t* smem, uint32_t w, uint32_t base, uint32_t (&out)[16]) {
+  uint32_t cp[8];
+  shifted_copies(w, cp);
+#define MSTF_G(J)                                                                 \
+  {                                                                               \
+    const uint32_t pc = __popc(w * (1u << (31 - 2 * J)));                         \
+    out[J] = ld_s32(smem, base + STRIDE * pc) & dibit_mask<J>(cp);                \
+  }
+  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
+  MSTF_G(8) MSTF_G(9) MSTF_G(10) MSTF_G(11) MSTF_G(12) MSTF_G(13) MSTF_G(14) MSTF_G(15)
+#undef MSTF_G
+}
+template <int STRIDE>
+__device__ __forceinline__ void gather8_s(const uint8_t* smem, uint32_t hw, uint32_t base, uint32_t (&out)[8]) {
+  uint32_t cp[8];
+  shifted_copies(hw, cp);
+#define MSTF_G(J)                                                                 \
+  {                                                                               \
+    const uint32_t pc = __popc(hw * (1u << (31 - 2 * J)));                        \
+    out[J] = ld_s32(smem, base + STRIDE * pc) & dibit_mask<J>(cp);                \
+  }
+  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
+#undef MSTF_G
+}
+
+template <int NK>
+__device__ __forceinline__ void fill_k3(const CompBlock& cb, uint8_t* smem, uint32_t (&kr)[2][16], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  build_interleaved<NK, false>(smem, cb.kval, cb.yk, cb.tok0, lane);
+  const uint32_t kw0 = g < cb.nvalid ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
+  const uint32_t kw1 = g + 8 < cb.nvalid ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
+  const uint32_t pk = __popc(kw0) | (__popc(kw1) << 16);
+  uint32_t ik = pk;
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
+    if (t >= o) ik += y;
+  }
+  const uint32_t ek = ik - pk;
+  __syncwarp();
+  const uint32_t b0 = cb.yk + 4u * (uint32_t)(KLayout<NK>::k0 + g) + 32u * (ek & 0xFFFF);
+  const uint32_t b1 = cb.yk + 4u * (uint32_t)(KLayout<NK>::k1 + g) + 32u * (ek >> 16);
+  gather16_s<32>(smem, kw0, b0, kr[0]);
+  gather16_s<32>(smem, kw1, b1, kr[1]);
+}
+
+template <int NV>
+__device__ __forceinline__ void fill_v3(const CompBlock& cb, uint8_t* smem, uint32_t (&vr)[4][8], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  build_interleaved<NV, true>(smem, cb.vval, cb.yv, cb.tok0, lane);
+  const uint32_t vw0 = g < cb.nvalid ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
+  const uint32_t vw1 = g + 8 < cb.nvalid ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
+  const uint32_t pv = __popc(vw0) | (__popc(vw1) << 16);
+  uint32_t iv = pv;
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o, 4);
+    if (t >= o) iv += y;
+  }
+  const uint32_t ev = iv - pv;
+  __syncwarp();
+  const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
+  const uint32_t w2t = __shfl_sync(0xffffffffu, vw0, sa), w2t8 = __shfl_sync(0xffffffffu, vw1, sa);
+  const uint32_t w2t1 = __shfl_sync(0xffffffffu, vw0, sb), w2t9 = __shfl_sync(0xffffffffu, vw1, sb);
+  const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
+  const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
+  const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
+  // token 2t+c: region r = (c & 1) + 2 * (c >> 3) = x for x = 0..3 (c = 0, 1, 8, 9), slot t
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
+    const uint32_t base = cb.yv + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * (ps[x] + extra);
+    gather8_s<16>(smem, ws[x] >> hsh, base, vr[x]);
+  }
+}
+
 // ---------------------------------------------------------------- dense source
 // 16 dense token rows of fp16 [*, kD] in global memory (window ring / dense KV baseline).
 struct DenseBlock {
@@ -243,10 +446,15 @@ struct WarpState {
 __device__ __forceinline__ void process_block(const BlockRegs& r, bool vg, bool vg8, WarpState& st,
                                               float scale_log2) {
   // ---- a5: scores S^T[tok][head] (rows tokens g, g+8; cols heads 2t, 2t+1)
-  float sc[4] = {0.f, 0.f, 0.f, 0.f};
+  float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};  // two chains hide HMMA latency
 #pragma unroll
-  for (int s = 0; s < 8; ++s)
+  for (int s = 0; s < 8; s += 2) {
     mma16816(sc, r.k[0][2 * s], r.k[1][2 * s], r.k[0][2 * s + 1], r.k[1][2 * s + 1], st.qf[2 * s], st.qf[2 * s + 1]);
+    mma16816(sd, r.k[0][2 * s + 2], r.k[1][2 * s + 2], r.k[0][2 * s + 3], r.k[1][2 * s + 3], st.qf[2 * s + 2],
+             st.qf[2 * s + 3]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) sc[i] += sd[i];
   // ---- a7: online softmax (log2 domain)
   const float x0 = vg ? sc[0] * scale_log2 : -INFINITY;
   const float x1 = vg ? sc[1] * scale_log2 : -INFINITY;
@@ -285,6 +493,66 @@ __device__ __forceinline__ void process_block(const BlockRegs& r, bool vg, bool 
       const uint32_t a2r = r.v[2 * kap + 1][i], a3r = r.v[2 * kap + 1][4 + i];
       mma16816(st.acc[0][i], a0r, a1r, a2r, a3r, be0, be1);
       mma16816(st.acc[1][i], a0r, a1r, a2r, a3r, bo0, bo1);
+    }
+  }
+}
+
+// K-warp state and block step: scores + online softmax; returns the V-warp handoff
+// {P^T fragment kappa 0, kappa 1, alpha head 2t, alpha head 2t+1}.
+struct KState {
+  float m0, m1, l0, l1;
+  uint32_t qf[16];
+};
+__device__ __forceinline__ uint4 k_block(const uint32_t (&kr)[2][16], bool vg, bool vg8, KState& st, float scale_log2) {
+  float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int s = 0; s < 8; s += 2) {
+    mma16816(sc, kr[0][2 * s], kr[1][2 * s], kr[0][2 * s + 1], kr[1][2 * s + 1], st.qf[2 * s], st.qf[2 * s + 1]);
+    mma16816(sd, kr[0][2 * s + 2], kr[1][2 * s + 2], kr[0][2 * s + 3], kr[1][2 * s + 3], st.qf[2 * s + 2],
+             st.qf[2 * s + 3]);
+  }
+  const float x0 = vg ? (sc[0] + sd[0]) * scale_log2 : -INFINITY;
+  const float x1 = vg ? (sc[1] + sd[1]) * scale_log2 : -INFINITY;
+  const float x2 = vg8 ? (sc[2] + sd[2]) * scale_log2 : -INFINITY;
+  const float x3 = vg8 ? (sc[3] + sd[3]) * scale_log2 : -INFINITY;
+  float bm0 = fmaxf(x0, x2), bm1 = fmaxf(x1, x3);
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
+    bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+  }
+  const float mn0 = fmaxf(st.m0, bm0), mn1 = fmaxf(st.m1, bm1);
+  const float a0 = exp2f(st.m0 - mn0), a1 = exp2f(st.m1 - mn1);
+  const float p0 = exp2f(x0 - mn0), p1 = exp2f(x1 - mn1), p2 = exp2f(x2 - mn0), p3 = exp2f(x3 - mn1);
+  st.l0 = st.l0 * a0 + (p0 + p2);
+  st.l1 = st.l1 * a1 + (p1 + p3);
+  st.m0 = mn0;
+  st.m1 = mn1;
+  return make_uint4(movmatrix_t(pack_half2(p0, p1)), movmatrix_t(pack_half2(p2, p3)), __float_as_uint(a0),
+                    __float_as_uint(a1));
+}
+
+// V-warp block step: rescale, then O^T += V-pairs . P (even / odd channel MMAs).
+__device__ __forceinline__ void v_block(const uint32_t (&vr)[4][8], const uint4 h, float (&acc)[2][4][4]) {
+  const float a0 = __uint_as_float(h.z), a1 = __uint_as_float(h.w);
+  if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[e][i][0] *= a0; acc[e][i][1] *= a1; acc[e][i][2] *= a0; acc[e][i][3] *= a1;
+      }
+  }
+  const uint32_t m[2] = {h.x, h.y};
+#pragma unroll
+  for (int kap = 0; kap < 2; ++kap) {
+    const uint32_t be0 = m[kap] & 0xFFFFu, be1 = m[kap] >> 16, bo0 = m[kap] << 16, bo1 = m[kap] & 0xFFFF0000u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t a0r = vr[2 * kap][i], a1r = vr[2 * kap][4 + i];
+      const uint32_t a2r = vr[2 * kap + 1][i], a3r = vr[2 * kap + 1][4 + i];
+      mma16816(acc[0][i], a0r, a1r, a2r, a3r, be0, be1);
+      mma16816(acc[1][i], a0r, a1r, a2r, a3r, bo0, bo1);
     }
   }
 }
@@ -454,29 +722,606 @@ __global__ void __launch_bounds__(kThreads, 2) mstf_attn_kernel(const AttnParams
   store_partial(st, p.ws_o, p.ws_ml, pidx, p.G, lane);
 }
 
+// ---------------------------------------------------------------- K2 (K/V warp-specialised)
+// 4 K-warps (0..3) + 4 V-warps (4..7) + 1 producer warp (8). K-warp w and V-warp w+4 share the
+// tokens [16w, 16w+16) of every stage: the K-warp gathers K, computes scores and the online
+// softmax and hands {P^T fragments, rescale factors} to its V-warp through a 2-slot shared
+// memory mailbox (mbarriers hfull / hempty); the V-warp gathers V and accumulates P.V.
+constexpr int kKVWarps = 8;
+constexpr int kThreadsKV = (kKVWarps + 1) * 32;
+constexpr int kBarBytesKV = 256;   // full[8], empty[8], hfull[8], hempty[8]
+constexpr int kHandoffBytes = 4 * 2 * 32 * 16;
+
+template <int NK, int NV, bool INTERLEAVED>
+__global__ void __launch_bounds__(kThreadsKV, 2) mstf_attn_kv_kernel(const AttnParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 8;
+  uint64_t* hfull = full + 16;
+  uint64_t* hempty = full + 24;
+  uint4* handoff = reinterpret_cast<uint4*>(smem + p.off_handoff);
+
+  const int u = blockIdx.y, split = blockIdx.x, S = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const CacheView& c = p.c;
+  const int n = c.n_comp[u];
+  const int chunks_total = (n + kChunk - 1) / kChunk;
+  const int cps = (chunks_total + S - 1) / S;
+  const int cbeg = min(split * cps, chunks_total), cend = min(cbeg + cps, chunks_total);
+  const int nchunks = cend - cbeg;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < p.nstage; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kKVWarps);
+    }
+    for (int i = 0; i < 8; ++i) {
+      mbar_init(&hfull[i], 1);
+      mbar_init(&hempty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kKVWarps) {
+    // ---------------- producer (same as the fused kernel)
+    if (lane == 0) {
+      const int kpk = c.kpad[0], kpv = c.kpad[1];
+      const uint8_t* kbm = reinterpret_cast<const uint8_t*>(c.bm[0] + (size_t)u * c.cap * kTiles);
+      const uint8_t* vbm = reinterpret_cast<const uint8_t*>(c.bm[1] + (size_t)u * c.cap * kTiles);
+      const uint8_t* kval = reinterpret_cast<const uint8_t*>(c.val[0] + (size_t)u * c.cap * kpk);
+      const uint8_t* vval = reinterpret_cast<const uint8_t*>(c.val[1] + (size_t)u * c.cap * kpv);
+      for (int i = 0; i < nchunks; ++i) {
+        const int st = i % p.nstage;
+        if (i >= p.nstage) mbar_wait(&empty[st], ((i / p.nstage) - 1) & 1);
+        const int tok0 = (cbeg + i) * kChunk;
+        const int nt = min(kChunk, n - tok0);
+        const uint32_t bbm = nt * 16, bk = nt * 2 * kpk, bv = nt * 2 * kpv;
+        uint8_t* sb = smem + kBarBytesKV + (size_t)st * p.stage_bytes;
+        mbar_arrive_expect_tx(&full[st], 2 * bbm + bk + bv);
+        bulk_g2s(sb, kbm + (size_t)tok0 * 16, bbm, &full[st]);
+        bulk_g2s(sb + p.off_kval, kval + (size_t)tok0 * 2 * kpk, bk, &full[st]);
+        bulk_g2s(sb + p.off_vbm, vbm + (size_t)tok0 * 16, bbm, &full[st]);
+        bulk_g2s(sb + p.off_vval, vval + (size_t)tok0 * 2 * kpv, bv, &full[st]);
+      }
+    }
+    return;
+  }
+
+  const bool is_k = warp < 4;
+  const int w = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  CompBlock cb;
+  cb.smem = smem;
+  cb.kpk = c.kpad[0];
+  cb.kpv = c.kpad[1];
+  cb.strk = 4 * cb.kpk + 16;
+  cb.strv = 4 * cb.kpv + 16;
+  cb.yk = p.off_pairs + (uint32_t)w * p.reg_k;
+  cb.yv = p.off_pairs + 4 * p.reg_k + (uint32_t)w * p.reg_v;
+  cb.tok0 = 16 * w;
+  const size_t pidx = ((size_t)u * S + split) * kConsumerWarps + w;
+  const int nwin_blocks = (split == S - 1 && c.W > 0) ? (c.W + 15) / 16 : 0;
+  const int nw = c.n_win[u];
+  const int first = c.W > 0 ? n % c.W : 0;
+
+  if (is_k) {
+    // ================= K-warp
+    KState st;
+    st.m0 = st.m1 = -INFINITY;
+    st.l0 = st.l1 = 0.f;
+    if (g < p.G) {
+      const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + g) * kD + 32 * t);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = qp[i];
+        st.qf[4 * i] = x.x; st.qf[4 * i + 1] = x.y; st.qf[4 * i + 2] = x.z; st.qf[4 * i + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) st.qf[i] = 0;
+    }
+    int blk = 0;
+    auto handoff_put = [&](const uint4 h) {
+      const int slot = blk & 1;
+      if (blk >= 2) mbar_wait(&hempty[2 * w + slot], ((blk >> 1) - 1) & 1);
+      handoff[(w * 2 + slot) * 32 + lane] = h;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hfull[2 * w + slot]);
+      ++blk;
+    };
+    for (int i = 0; i < nchunks; ++i) {
+      const int sidx = i % p.nstage;
+      mbar_wait(&full[sidx], (i / p.nstage) & 1);
+      const uint32_t sb = kBarBytesKV + (uint32_t)sidx * p.stage_bytes;
+      const int nvalid = min(16, n - (cbeg + i) * kChunk - 16 * w);
+      uint32_t kr[2][16];
+      if (nvalid > 0) {
+        cb.kbm = sb;
+        cb.kval = sb + p.off_kval;
+        cb.nvalid = nvalid;
+        if constexpr (INTERLEAVED && NK > 0) fill_k3<NK>(cb, smem, kr, lane); else fill_k<NK>(cb, smem, kr, lane);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sidx]);
+      if (nvalid > 0) handoff_put(k_block(kr, g < nvalid, g + 8 < nvalid, st, p.scale_log2));
+    }
+    for (int blkw = w; blkw < nwin_blocks; blkw += 4) {
+      DenseBlock db;
+      db.k = c.win[0] + (size_t)u * c.W * kD;
+      db.v = c.win[1] + (size_t)u * c.W * kD;
+      db.ring = true; db.row0 = blkw * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
+      bool any = false;
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
+      if (!any) continue;
+      uint32_t kr[2][16];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int tok = g + 8 * x;
+        if (db.valid(tok)) {
+          const uint4* pp = reinterpret_cast<const uint4*>(db.k + (size_t)(db.row0 + tok) * kD + 32 * t);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 a = pp[j];
+            kr[x][4 * j] = a.x; kr[x][4 * j + 1] = a.y; kr[x][4 * j + 2] = a.z; kr[x][4 * j + 3] = a.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) kr[x][j] = 0;
+        }
+      }
+      handoff_put(k_block(kr, db.valid(g), db.valid(g + 8), st, p.scale_log2));
+    }
+    // partial (m, l)
+    float l0 = st.l0, l1 = st.l1;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    float* ml = p.ws_ml + pidx * p.G * 2;
+    if (g == 0) {
+      if (2 * t < p.G) { ml[4 * t] = st.m0; ml[4 * t + 1] = l0; }
+      if (2 * t + 1 < p.G) { ml[4 * t + 2] = st.m1; ml[4 * t + 3] = l1; }
+    }
+  } else {
+    // ================= V-warp
+    float acc[2][4][4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[e][i][0] = acc[e][i][1] = acc[e][i][2] = acc[e][i][3] = 0.f;
+    int blk = 0;
+    auto handoff_get = [&]() -> uint4 {
+      const int slot = blk & 1;
+      mbar_wait(&hfull[2 * w + slot], (blk >> 1) & 1);
+      const uint4 h = handoff[(w * 2 + slot) * 32 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hempty[2 * w + slot]);
+      ++blk;
+      return h;
+    };
+    for (int i = 0; i < nchunks; ++i) {
+      const int sidx = i % p.nstage;
+      mbar_wait(&full[sidx], (i / p.nstage) & 1);
+      const uint32_t sb = kBarBytesKV + (uint32_t)sidx * p.stage_bytes;
+      const int nvalid = min(16, n - (cbeg + i) * kChunk - 16 * w);
+      uint32_t vr[4][8];
+      if (nvalid > 0) {
+        cb.vbm = sb + p.off_vbm;
+        cb.vval = sb + p.off_vval;
+        cb.nvalid = nvalid;
+        if constexpr (INTERLEAVED && NV > 0) fill_v3<NV>(cb, smem, vr, lane); else fill_v<NV>(cb, smem, vr, lane);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sidx]);
+      if (nvalid > 0) v_block(vr, handoff_get(), acc);
+    }
+    for (int blkw = w; blkw < nwin_blocks; blkw += 4) {
+      DenseBlock db;
+      db.k = c.win[0] + (size_t)u * c.W * kD;
+      db.v = c.win[1] + (size_t)u * c.W * kD;
+      db.ring = true; db.row0 = blkw * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
+      bool any = false;
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
+      if (!any) continue;
+      uint32_t vr[4][8];
+      const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        if (db.valid(tk[x])) {
+          const uint4* pp = reinterpret_cast<const uint4*>(db.v + (size_t)(db.row0 + tk[x]) * kD + 16 * g);
+          const uint4 a = pp[0], b = pp[1];
+          vr[x][0] = a.x; vr[x][1] = a.y; vr[x][2] = a.z; vr[x][3] = a.w;
+          vr[x][4] = b.x; vr[x][5] = b.y; vr[x][6] = b.z; vr[x][7] = b.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) vr[x][j] = 0;
+        }
+      }
+      v_block(vr, handoff_get(), acc);
+    }
+    float* o = p.ws_o + pidx * p.G * kD;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int h = 2 * t + hh;
+      if (h < p.G) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          *reinterpret_cast<float2*>(o + h * kD + 16 * g + 2 * i) = make_float2(acc[0][i][hh], acc[1][i][hh]);
+          *reinterpret_cast<float2*>(o + h * kD + 16 * g + 8 + 2 * i) =
+              make_float2(acc[0][i][2 + hh], acc[1][i][2 + hh]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fused split combine (a9)
+// Called by every thread of a CTA after its warps stored their partials. The last CTA of the unit
+// (ticket counter in the workspace) merges the S * 4 partials and writes the output; the ticket
+// is reset to 0 so the workspace is reusable (it must be zeroed once before first use).
+__device__ __forceinline__ void combine_if_last(const AttnParams& p, int u, int S, void* out, int out_f16) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(p.tickets + u, 1);
+    s_last = (prev == S - 1);
+    if (s_last) p.tickets[u] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int nparts = S * kConsumerWarps;
+  const int G = p.G;
+  const int nthreads = blockDim.x;
+  // one warp per head; lane owns channels 4*lane..4*lane+3
+  for (int h = threadIdx.x >> 5; h < G; h += nthreads >> 5) {
+    const int lane = threadIdx.x & 31;
+    float M = -INFINITY;
+    for (int i = lane; i < nparts; i += 32) M = fmaxf(M, __ldcg(p.ws_ml + (((size_t)u * nparts + i) * G + h) * 2));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int i = 0; i < nparts; ++i) {
+      const size_t pi = (size_t)u * nparts + i;
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (pi * G + h) * 2));
+      const float4 o = __ldcg(reinterpret_cast<const float4*>(p.ws_o + (pi * G + h) * kD + 4 * lane));
+      const float wgt = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
+      L += wgt * ml.y;
+      acc.x += wgt * o.x; acc.y += wgt * o.y; acc.z += wgt * o.z; acc.w += wgt * o.w;
+    }
+    const float inv = 1.f / L;
+    const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
+    if (out_f16) {
+      __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(out) + oi);
+      po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
+      po[1] = __floats2half2_rn(acc.z * inv, acc.w * inv);
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + oi) =
+          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2 v4: register-staged (no TMA ring)
+// 4 K-warps + 4 V-warps per CTA; K-warp w and V-warp w+4 own the 16-token blocks
+// b = w, w+4, w+8, ... of the split. Each warp loads its tensor's packed values and bitmap
+// words for the NEXT block with 64/32-bit global loads into registers (software pipelining),
+// then builds the interleaved pair arrays from registers (no shared-memory staging reads).
+template <int NCH>
+struct RawRegs {
+  static constexpr int nw = PairGeom<NCH>::nw;
+  uint32_t W[nw];
+  uint32_t bm0, bm1;  // bitmap word t of tokens g, g+8
+};
+
+template <int NCH>
+__device__ __forceinline__ void load_raw(RawRegs<NCH>& rr, const uint16_t* __restrict__ vals,
+                                         const uint64_t* __restrict__ bms, int tok0, int nvalid, int lane) {
+  using Gm = PairGeom<NCH>;
+  const int tau = lane >> 1, h = lane & 1, g = lane >> 2, t = lane & 3;
+  const int m0 = h ? Gm::kp / 2 + 2 : 0;
+  // words wb .. wb + nw - 1 of token tok0 + tau, wb = m0/2 - 1 (h = 0: word -1 is zero)
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(vals + (size_t)(tok0 + tau) * Gm::kp) + (m0 / 2 - 1);
+  const bool ok = tau < nvalid;
+  rr.W[0] = (h && ok) ? __ldg(src) : 0u;
+#pragma unroll
+  for (int i = 1; i < Gm::nw; ++i) rr.W[i] = ok ? __ldg(src + i) : 0u;
+  const uint32_t* bw = reinterpret_cast<const uint32_t*>(bms);
+  rr.bm0 = g < nvalid ? __ldg(bw + (size_t)(tok0 + g) * 4 + t) : 0u;
+  rr.bm1 = g + 8 < nvalid ? __ldg(bw + (size_t)(tok0 + g + 8) * 4 + t) : 0u;
+}
+
+template <int NCH, bool IS_V>
+__device__ __forceinline__ void store_pairs(uint8_t* smem, const RawRegs<NCH>& rr, uint32_t ybase, int lane) {
+  using Gm = PairGeom<NCH>;
+  const int tau = lane >> 1, h = lane & 1;
+  const int m0 = h ? Gm::kp / 2 + 2 : 0;
+  uint32_t dst, step;
+  if (IS_V) {
+    const int r = (tau & 1) + 2 * (tau >> 3);
+    dst = ybase + 4u * (uint32_t)(VLayout<NCH>::region(r) + ((tau >> 1) & 3) + 4 * m0);
+    step = 16;
+  } else {
+    dst = ybase + 4u * (uint32_t)((tau >> 3 ? KLayout<NCH>::k1 : KLayout<NCH>::k0) + (tau & 7) + 8 * m0);
+    step = 32;
+  }
+#pragma unroll
+  for (int e = 0; e < Gm::E; ++e) {
+    const uint32_t y = (e & 1) ? rr.W[(e + 1) >> 1] : prmt(rr.W[e >> 1], rr.W[(e >> 1) + 1], 0x5432);
+    *reinterpret_cast<uint32_t*>(smem + dst + step * e) = y;
+  }
+}
+
+template <int NK, int NV>
+__global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* hempty = hfull + 8;
+  uint4* handoff = reinterpret_cast<uint4*>(smem + 128);
+
+  const int u = blockIdx.y, split = blockIdx.x, S = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const CacheView& c = p.c;
+  const int n = c.n_comp[u];
+  // split the unit's 16-token blocks contiguously over the S CTAs
+  const int blocks_total = (n + 15) / 16;
+  const int bps = (blocks_total + S - 1) / S;
+  const int bbeg = min(split * bps, blocks_total), bend = min(bbeg + bps, blocks_total);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) {
+      mbar_init(&hfull[i], 1);
+      mbar_init(&hempty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const bool is_k = warp < 4;
+  const int w = warp & 3;
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t ybase = p.off_pairs + (is_k ? (uint32_t)w * p.reg_k : 4 * p.reg_k + (uint32_t)w * p.reg_v);
+  const size_t pidx = ((size_t)u * S + split) * kConsumerWarps + w;
+  const int nwin_blocks = (split == S - 1 && c.W > 0) ? (c.W + 15) / 16 : 0;
+  const int nw = c.n_win[u];
+  const int first = c.W > 0 ? n % c.W : 0;
+
+  if (is_k) {
+    // ================= K-warp
+    const uint16_t* vals = c.val[0] + (size_t)u * c.cap * c.kpad[0];
+    const uint64_t* bms = c.bm[0] + (size_t)u * c.cap * kTiles;
+    KState st;
+    st.m0 = st.m1 = -INFINITY;
+    st.l0 = st.l1 = 0.f;
+    if (g < p.G) {
+      const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + g) * kD + 32 * t);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = qp[i];
+        st.qf[4 * i] = x.x; st.qf[4 * i + 1] = x.y; st.qf[4 * i + 2] = x.z; st.qf[4 * i + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) st.qf[i] = 0;
+    }
+    int blk = 0;
+    auto handoff_put = [&](const uint4 hh) {
+      const int slot = blk & 1;
+      if (blk >= 2) mbar_wait(&hempty[2 * w + slot], ((blk >> 1) - 1) & 1);
+      handoff[(w * 2 + slot) * 32 + lane] = hh;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hfull[2 * w + slot]);
+      ++blk;
+    };
+    auto k_step = [&](const RawRegs<NK>& cur, int b) {
+      const int nvalid = min(16, n - b * 16);
+      __syncwarp();
+      store_pairs<NK, false>(smem, cur, ybase, lane);
+      const uint32_t pk = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
+      uint32_t ik = pk;
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
+        if (t >= o) ik += y;
+      }
+      const uint32_t ek = ik - pk;
+      __syncwarp();
+      uint32_t kr[2][16];
+      gather16_s<32>(smem, cur.bm0, ybase + 4u * (uint32_t)(KLayout<NK>::k0 + g) + 32u * (ek & 0xFFFF), kr[0]);
+      gather16_s<32>(smem, cur.bm1, ybase + 4u * (uint32_t)(KLayout<NK>::k1 + g) + 32u * (ek >> 16), kr[1]);
+      handoff_put(k_block(kr, g < nvalid, g + 8 < nvalid, st, p.scale_log2));
+    };
+    {
+      RawRegs<NK> ra, rb;
+      int b = bbeg + w;
+      if (b < bend) load_raw<NK>(ra, vals, bms, b * 16, min(16, n - b * 16), lane);
+      while (b < bend) {
+        if (b + 4 < bend) load_raw<NK>(rb, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
+        k_step(ra, b);
+        b += 4;
+        if (b >= bend) break;
+        if (b + 4 < bend) load_raw<NK>(ra, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
+        k_step(rb, b);
+        b += 4;
+      }
+    }
+    for (int blkw = w; blkw < nwin_blocks; blkw += 4) {
+      DenseBlock db;
+      db.k = c.win[0] + (size_t)u * c.W * kD;
+      db.v = c.win[1] + (size_t)u * c.W * kD;
+      db.ring = true; db.row0 = blkw * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
+      bool any = false;
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
+      if (!any) continue;
+      uint32_t kr[2][16];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int tok = g + 8 * x;
+        if (db.valid(tok)) {
+          const uint4* pp = reinterpret_cast<const uint4*>(db.k + (size_t)(db.row0 + tok) * kD + 32 * t);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 a = pp[j];
+            kr[x][4 * j] = a.x; kr[x][4 * j + 1] = a.y; kr[x][4 * j + 2] = a.z; kr[x][4 * j + 3] = a.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) kr[x][j] = 0;
+        }
+      }
+      handoff_put(k_block(kr, db.valid(g), db.valid(g + 8), st, p.scale_log2));
+    }
+    float l0 = st.l0, l1 = st.l1;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    float* ml = p.ws_ml + pidx * p.G * 2;
+    if (g == 0) {
+      if (2 * t < p.G) { ml[4 * t] = st.m0; ml[4 * t + 1] = l0; }
+      if (2 * t + 1 < p.G) { ml[4 * t + 2] = st.m1; ml[4 * t + 3] = l1; }
+    }
+  } else {
+    // ================= V-warp
+    const uint16_t* vals = c.val[1] + (size_t)u * c.cap * c.kpad[1];
+    const uint64_t* bms = c.bm[1] + (size_t)u * c.cap * kTiles;
+    float acc[2][4][4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[e][i][0] = acc[e][i][1] = acc[e][i][2] = acc[e][i][3] = 0.f;
+    int blk = 0;
+    auto handoff_get = [&]() -> uint4 {
+      const int slot = blk & 1;
+      mbar_wait(&hfull[2 * w + slot], (blk >> 1) & 1);
+      const uint4 hh = handoff[(w * 2 + slot) * 32 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hempty[2 * w + slot]);
+      ++blk;
+      return hh;
+    };
+    auto v_step = [&](const RawRegs<NV>& cur) {
+      __syncwarp();
+      store_pairs<NV, true>(smem, cur, ybase, lane);
+      const uint32_t pv = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
+      uint32_t iv = pv;
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o, 4);
+        if (t >= o) iv += y;
+      }
+      const uint32_t ev = iv - pv;
+      __syncwarp();
+      const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
+      const uint32_t w2t = __shfl_sync(0xffffffffu, cur.bm0, sa), w2t8 = __shfl_sync(0xffffffffu, cur.bm1, sa);
+      const uint32_t w2t1 = __shfl_sync(0xffffffffu, cur.bm0, sb), w2t9 = __shfl_sync(0xffffffffu, cur.bm1, sb);
+      const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
+      const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
+      const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
+      uint32_t vr[4][8];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
+        const uint32_t base = ybase + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * (ps[x] + extra);
+        gather8_s<16>(smem, ws[x] >> hsh, base, vr[x]);
+      }
+      v_block(vr, handoff_get(), acc);
+    };
+    {
+      RawRegs<NV> ra, rb;
+      int b = bbeg + w;
+      if (b < bend) load_raw<NV>(ra, vals, bms, b * 16, min(16, n - b * 16), lane);
+      while (b < bend) {
+        if (b + 4 < bend) load_raw<NV>(rb, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
+        v_step(ra);
+        b += 4;
+        if (b >= bend) break;
+        if (b + 4 < bend) load_raw<NV>(ra, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
+        v_step(rb);
+        b += 4;
+      }
+    }
+    for (int blkw = w; blkw < nwin_blocks; blkw += 4) {
+      DenseBlock db;
+      db.k = c.win[0] + (size_t)u * c.W * kD;
+      db.v = c.win[1] + (size_t)u * c.W * kD;
+      db.ring = true; db.row0 = blkw * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
+      bool any = false;
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
+      if (!any) continue;
+      uint32_t vr[4][8];
+      const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        if (db.valid(tk[x])) {
+          const uint4* pp = reinterpret_cast<const uint4*>(db.v + (size_t)(db.row0 + tk[x]) * kD + 16 * g);
+          const uint4 a = pp[0], bb = pp[1];
+          vr[x][0] = a.x; vr[x][1] = a.y; vr[x][2] = a.z; vr[x][3] = a.w;
+          vr[x][4] = bb.x; vr[x][5] = bb.y; vr[x][6] = bb.z; vr[x][7] = bb.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) vr[x][j] = 0;
+        }
+      }
+      v_block(vr, handoff_get(), acc);
+    }
+    float* o = p.ws_o + pidx * p.G * kD;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int h = 2 * t + hh;
+      if (h < p.G) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          *reinterpret_cast<float2*>(o + h * kD + 16 * g + 2 * i) = make_float2(acc[0][i][hh], acc[1][i][hh]);
+          *reinterpret_cast<float2*>(o + h * kD + 16 * g + 8 + 2 * i) =
+              make_float2(acc[0][i][2 + hh], acc[1][i][2 + hh]);
+        }
+      }
+    }
+  }
+  combine_if_last(p, u, S, p.out, p.out_f16);
+}
+
 // ---------------------------------------------------------------- K3: combine partials
 __global__ void mstf_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int nparts,
                                     int G, void* out, int out_f16) {
-  const int u = blockIdx.x;
-  const int h = threadIdx.x / kD, ch = threadIdx.x % kD;
+  // one warp per (unit, head); lane owns channels 4*lane .. 4*lane+3
+  const int u = blockIdx.x, h = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (h >= G) return;
   float M = -INFINITY;
-  for (int i = 0; i < nparts; ++i) M = fmaxf(M, ws_ml[(((size_t)u * nparts + i) * G + h) * 2]);
-  float L = 0.f, acc = 0.f;
+  for (int i = lane; i < nparts; i += 32) M = fmaxf(M, ws_ml[(((size_t)u * nparts + i) * G + h) * 2]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
   for (int i = 0; i < nparts; ++i) {
     const size_t pi = (size_t)u * nparts + i;
-    const float m = ws_ml[(pi * G + h) * 2];
-    if (m == -INFINITY) continue;
-    const float w = exp2f(m - M);
-    L += w * ws_ml[(pi * G + h) * 2 + 1];
-    acc += w * ws_o[(pi * G + h) * kD + ch];
+    const float2 ml = *reinterpret_cast<const float2*>(ws_ml + (pi * G + h) * 2);
+    const float4 o = *reinterpret_cast<const float4*>(ws_o + (pi * G + h) * kD + 4 * lane);
+    const float w = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
+    L += w * ml.y;
+    acc.x += w * o.x; acc.y += w * o.y; acc.z += w * o.z; acc.w += w * o.w;
   }
-  const float o = acc / L;
-  const size_t oi = ((size_t)u * G + h) * kD + ch;
-  if (out_f16)
-    reinterpret_cast<__half*>(out)[oi] = __float2half_rn(o);
-  else
-    reinterpret_cast<float*>(out)[oi] = o;
+  const float inv = 1.f / L;
+  const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
+  if (out_f16) {
+    __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(out) + oi);
+    po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
+    po[1] = __floats2half2_rn(acc.z * inv, acc.w * inv);
+  } else {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + oi) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  }
 }
 
 // ---------------------------------------------------------------- dense baseline
@@ -509,29 +1354,62 @@ __global__ void __launch_bounds__(kConsumerWarps * 32) mstf_dense_attn_kernel(
 // ---------------------------------------------------------------- host side
 int32_t max_splits_for(int32_t U, int32_t capacity) {
   const int32_t chunks = (capacity + kChunk - 1) / kChunk;
-  int32_t s = (4 * 148 + U - 1) / U;
+  int32_t s = (8 * 148 + U - 1) / U;  // plan_attention: <= ~4 waves of 2 CTAs per SM (148 SMs)
+  if (s > 64) s = 64;
   if (s > chunks) s = chunks;
   return s < 1 ? 1 : s;
 }
 
+static size_t ticket_bytes(int32_t U) { return ((size_t)U * sizeof(int) + 255) / 256 * 256; }
+
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits) {
   const size_t parts = (size_t)U * max_splits * kConsumerWarps;
-  return parts * G * (kD + 2) * sizeof(float) + 256;
+  return ticket_bytes(U) + parts * G * (kD + 2) * sizeof(float) + 256;
+}
+
+// Bytes of one warp's pair-array region: max of the contiguous layout (generic kernels) and
+// the interleaved layout (templated kernels), rounded to 128 B (bank offset 0).
+static int32_t pair_region_bytes(int32_t kp, bool v) {
+  const int32_t contiguous = 16 * (4 * kp + 16);
+  const int32_t rows = kp + 4;
+  int32_t words;
+  if (!v) {
+    const int32_t k1 = pad_to_bank(8 * rows, 8);
+    words = k1 + 8 * rows;
+  } else {
+    const int32_t v1 = pad_to_bank(4 * rows, 4);
+    const int32_t v2 = pad_to_bank(v1 + 4 * rows, 16);
+    const int32_t v3 = pad_to_bank(v2 + 4 * rows, 20);
+    words = v3 + 4 * rows;
+  }
+  const int32_t inter = 4 * words;
+  const int32_t b = contiguous > inter ? contiguous : inter;
+  return (b + 127) / 128 * 128;
 }
 
 AttnPlan plan_attention(int32_t U, int32_t max_comp, int32_t kpad_k, int32_t kpad_v, int32_t sm_count) {
   AttnPlan pl;
   pl.stage_bytes = kChunk * (16 + 2 * kpad_k + 16 + 2 * kpad_v);
-  pl.pair_bytes = kConsumerWarps * 16 * ((4 * kpad_k + 16) + (4 * kpad_v + 16));
+  pl.reg_k = pair_region_bytes(kpad_k, false);
+  pl.reg_v = pair_region_bytes(kpad_v, true);
+  pl.pair_bytes = kConsumerWarps * (pl.reg_k + pl.reg_v);
   // two CTAs per SM when it fits: ~110 KB per CTA for stages + pair arrays
-  int ns = (110 * 1024 - pl.pair_bytes - kBarBytesHost) / pl.stage_bytes;
+  int ns = (110 * 1024 - pl.pair_bytes - 256 - 4096) / pl.stage_bytes;
   pl.nstage = ns < 2 ? 2 : (ns > 4 ? 4 : ns);
   const int32_t chunks = (max_comp + kChunk - 1) / kChunk;
-  int32_t target = 3 * sm_count;
-  int32_t s = (target + U - 1) / U;
-  const int32_t cap_s = chunks / 2 > 1 ? chunks / 2 : 1;  // >= 2 chunks per split
-  if (s > cap_s) s = cap_s;
-  pl.splits = s < 1 ? 1 : s;
+  // Split count: minimise waves(U*S / (2 CTAs per SM)) x (chunks per CTA + c0), where c0 ~ 2 chunks
+  // is the measured per-CTA fixed cost (prologue, first loads, epilogue; tools/split_scan.py).
+  const int32_t slots = 2 * sm_count;
+  const int32_t cap_s = chunks > 1 ? chunks : 1;
+  int32_t best = 1;
+  double best_t = 1e30;
+  const int32_t max_s = (4 * slots + U - 1) / U;  // at most ~4 waves
+  for (int32_t s = 1; s <= cap_s && s <= max_s && s <= 64; ++s) {
+    const double waves = std::ceil((double)U * s / slots);
+    const double t = waves * ((double)chunks / s + 2.0);
+    if (t < best_t - 1e-9) { best_t = t; best = s; }
+  }
+  pl.splits = best;
   return pl;
 }
 
@@ -547,29 +1425,51 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.off_kval = kChunk * 16;
   p.off_vbm = p.off_kval + kChunk * 2 * c.kpad[0];
   p.off_vval = p.off_vbm + kChunk * 16;
-  p.off_pairs = kBarBytes + plan.nstage * plan.stage_bytes;
+  p.off_pairs = kBarBytesKV + plan.nstage * plan.stage_bytes;
+  p.off_handoff = p.off_pairs + plan.pair_bytes;
+  p.reg_k = plan.reg_k;
+  p.reg_v = plan.reg_v;
   const size_t parts = (size_t)c.U * plan.splits * kConsumerWarps;
-  p.ws_o = reinterpret_cast<float*>(ws);
+  p.tickets = reinterpret_cast<int*>(ws);  // [U] ticket counters at a fixed place (zero between calls)
+  p.ws_o = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ticket_bytes(c.U));
   p.ws_ml = p.ws_o + parts * G * kD;
-  const int smem = kBarBytes + plan.nstage * plan.stage_bytes + plan.pair_bytes;
-  void (*kern)(AttnParams) = mstf_attn_kernel<0, 0>;
+  p.out = out;
+  p.out_f16 = out_f16;
+  const int smem = kBarBytesKV + plan.nstage * plan.stage_bytes + plan.pair_bytes + kHandoffBytes;
+  // kernel choice: register-staged interleaved kernel for kpad <= 40 (nk <= 5); TMA-staged kernel
+  // with contiguous pair arrays for kpad >= 48 (interleaving aliases banks at ~50% density).
+  void (*kern)(AttnParams) = mstf_attn_kv_kernel<0, 0, false>;
   const int nk = c.kpad[0] / 8, nv = c.kpad[1] / 8;
   if (nk == nv) {
     switch (nk) {
-      case 2: kern = mstf_attn_kernel<2, 2>; break;
-      case 4: kern = mstf_attn_kernel<4, 4>; break;
-      case 5: kern = mstf_attn_kernel<5, 5>; break;
-      case 8: kern = mstf_attn_kernel<8, 8>; break;
-      case 16: kern = mstf_attn_kernel<16, 16>; break;
+      case 8: kern = mstf_attn_kv_kernel<8, 8, false>; break;
+      case 16: kern = mstf_attn_kv_kernel<16, 16, false>; break;
       default: break;
     }
   }
+  const char* kv = std::getenv("MSTF_KERNEL");
+  const bool use_reg = (nk == nv) && (nk == 2 || nk == 4 || nk == 5) && !(kv && kv[0] == 't');
+  if (use_reg) {
+    void (*rk)(AttnParams) = nullptr;
+    switch (nk) {
+      case 2: rk = mstf_attn_reg_kernel<2, 2>; break;
+      case 4: rk = mstf_attn_reg_kernel<4, 4>; break;
+      default: rk = mstf_attn_reg_kernel<5, 5>; break;
+    }
+    AttnParams pr = p;
+    pr.off_pairs = 128 + kHandoffBytes;
+    const int rsmem = pr.off_pairs + plan.pair_bytes;
+    cudaError_t e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
+    if (e != cudaSuccess) return e;
+    rk<<<dim3(plan.splits, c.U), 256, rsmem, s>>>(pr);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(plan.splits, c.U), kThreads, smem, s>>>(p);
+  kern<<<dim3(plan.splits, c.U), kThreadsKV, smem, s>>>(p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  mstf_combine_kernel<<<c.U, G * kD, 0, s>>>(p.ws_o, p.ws_ml, plan.splits * kConsumerWarps, G, out, out_f16);
+  mstf_combine_kernel<<<c.U, G * 32, 0, s>>>(p.ws_o, p.ws_ml, plan.splits * kConsumerWarps, G, out, out_f16);
   return cudaGetLastError();
 }
 
@@ -583,7 +1483,7 @@ cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const i
                                                                         scale * 1.4426950408889634f, ws_o, ws_ml);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  mstf_combine_kernel<<<U, G * kD, 0, s>>>(ws_o, ws_ml, splits * kConsumerWarps, G, out, out_f16);
+  mstf_combine_kernel<<<U, G * 32, 0, s>>>(ws_o, ws_ml, splits * kConsumerWarps, G, out, out_f16);
   return cudaGetLastError();
 }
 

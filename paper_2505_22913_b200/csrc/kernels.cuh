@@ -36,6 +36,7 @@ struct AttnPlan {
   int32_t nstage;        // TMA ring depth
   int32_t stage_bytes;   // bytes of one stage (K bm, K vals, V bm, V vals for kChunk tokens)
   int32_t pair_bytes;    // per-CTA shifted pair arrays (4 warps x 16 tokens x K,V)
+  int32_t reg_k, reg_v;  // per-warp region bytes
 };
 AttnPlan plan_attention(int32_t U, int32_t max_comp, int32_t kpad_k, int32_t kpad_v, int32_t sm_count);
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits);

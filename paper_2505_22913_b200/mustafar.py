@@ -156,7 +156,7 @@ class MustafarCache:
         h = ctypes.c_void_p()
         _check("mstf_cache_create", lib().mstf_cache_create(ctypes.byref(self.cfg), ptrs, ctypes.byref(h)))
         self._h = h
-        self._ws = torch.empty(max(int(lib().mstf_workspace_bytes(self._h)), 256), dtype=torch.uint8,
+        self._ws = torch.zeros(max(int(lib().mstf_workspace_bytes(self._h)), 256), dtype=torch.uint8,
                                device=self.device)
         self.keep_k, self.keep_v, self.window, self.capacity = keep_k, keep_v, window, capacity
 
