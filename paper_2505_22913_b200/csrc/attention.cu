@@ -97,6 +97,22 @@ struct CompBlock {
   uint32_t strk, strv;   // pair-array stride per token (bytes)
 };
 
+// Materialise a value in one register (stops the compiler from re-associating base + stride * pc
+// into several adds per gather).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  asm("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
+// 32-bit shared-window loads / stores (absolute shared addresses, no generic->shared conversion).
+__device__ __forceinline__ uint32_t lds_abs(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_abs(uint32_t saddr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_s32(const uint8_t* smem, uint32_t off) {
   return *reinterpret_cast<const uint32_t*>(smem + off);
 }
@@ -313,26 +329,28 @@ __device__ __forceinline__ void build_interleaved(uint8_t* smem, uint32_t raw, u
 
 // Expand 16 dibits of word w; entry r of this token's pair array at base + stride * r.
 template <int STRIDE>
-__device__ __forceinline__ void gather16_s(const uint8_t* smem, uint32_t w, uint32_t base, uint32_t (&out)[16]) {
+__device__ __forceinline__ void gather16_s(const uint8_t* smem, uint32_t w, uint32_t base_in, uint32_t (&out)[16]) {
+  const uint32_t base = opaque(base_in + smem_u32(smem));
   uint32_t cp[8];
   shifted_copies(w, cp);
 #define MSTF_G(J)                                                                 \
   {                                                                               \
     const uint32_t pc = __popc(w * (1u << (31 - 2 * J)));                         \
-    out[J] = ld_s32(smem, base + STRIDE * pc) & dibit_mask<J>(cp);                \
+    out[J] = lds_abs(base + STRIDE * pc) & dibit_mask<J>(cp);                      \
   }
   MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
   MSTF_G(8) MSTF_G(9) MSTF_G(10) MSTF_G(11) MSTF_G(12) MSTF_G(13) MSTF_G(14) MSTF_G(15)
 #undef MSTF_G
 }
 template <int STRIDE>
-__device__ __forceinline__ void gather8_s(const uint8_t* smem, uint32_t hw, uint32_t base, uint32_t (&out)[8]) {
+__device__ __forceinline__ void gather8_s(const uint8_t* smem, uint32_t hw, uint32_t base_in, uint32_t (&out)[8]) {
+  const uint32_t base = opaque(base_in + smem_u32(smem));
   uint32_t cp[8];
   shifted_copies(hw, cp);
 #define MSTF_G(J)                                                                 \
   {                                                                               \
     const uint32_t pc = __popc(hw * (1u << (31 - 2 * J)));                        \
-    out[J] = ld_s32(smem, base + STRIDE * pc) & dibit_mask<J>(cp);                \
+    out[J] = lds_abs(base + STRIDE * pc) & dibit_mask<J>(cp);                      \
   }
   MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
 #undef MSTF_G
@@ -1052,10 +1070,11 @@ __device__ __forceinline__ void store_pairs(uint8_t* smem, const RawRegs<NCH>& r
     dst = ybase + 4u * (uint32_t)((tau >> 3 ? KLayout<NCH>::k1 : KLayout<NCH>::k0) + (tau & 7) + 8 * m0);
     step = 32;
   }
+  const uint32_t adst = opaque(dst + smem_u32(smem));
 #pragma unroll
   for (int e = 0; e < Gm::E; ++e) {
     const uint32_t y = (e & 1) ? rr.W[(e + 1) >> 1] : prmt(rr.W[e >> 1], rr.W[(e >> 1) + 1], 0x5432);
-    *reinterpret_cast<uint32_t*>(smem + dst + step * e) = y;
+    sts_abs(adst + step * e, y);
   }
 }
 
