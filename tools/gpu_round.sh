@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round measurement script (run under gpurun): tests, bench lines, launch list, ncu capture.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/smi.txt
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
+for w in C2_s50 C3 C4 C5; do
+  timeout 600 python bench.py --steps 5 --warmup 3 --workload $w --no-cpu-baseline > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
+done
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:mstf --csv \
+   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-dense --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:mstf_attn -s 40 -c 1 \
+   -o gpurun_out/prof_bench python bench.py --steps 2 --warmup 3 --no-dense --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+ls -la gpurun_out
