@@ -166,12 +166,22 @@ int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale
   if (out_dtype != MSTF_OUT_F32 && out_dtype != MSTF_OUT_F16) return MSTF_EINVAL;
   if (!ws || !aligned16(ws) || ws_bytes < mstf_workspace_bytes(h)) return MSTF_EWORKSPACE;
   int32_t max_comp = 0;
+  int64_t total_items = 0;
+  const int32_t nwb = h->view.W > 0 ? (h->view.W + 15) / 16 : 0;
+  int32_t uniform_items = (h->nc[0] + 15) / 16 + nwb;
   for (int32_t u = 0; u < h->view.U; ++u) {
     if (h->nc[u] + h->nw[u] == 0) return MSTF_EEMPTY;
     if (h->nc[u] > max_comp) max_comp = h->nc[u];
+    const int32_t items = (h->nc[u] + 15) / 16 + nwb;
+    total_items += items;
+    if (items != uniform_items) uniform_items = 0;
   }
   const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
-  AttnPlan plan = plan_attention(h->view.U, max_comp, h->view.kpad[0], h->view.kpad[1], sm_count());
+  AttnPlan plan = plan_attention(h->view.U, max_comp, total_items, uniform_items, h->view.kpad[0],
+                                 h->view.kpad[1], sm_count());
+  if (const char* env = std::getenv("MSTF_SCHED")) {  // tuning override: "split" forces the split grid
+    if (std::strcmp(env, "split") == 0) plan.sk = 0;
+  }
   if (const char* env = std::getenv("MSTF_SPLITS")) {  // tuning override (not part of the ABI contract)
     const int v = std::atoi(env);
     if (v > 0) plan.splits = v;
@@ -232,6 +242,10 @@ const char* mstf_status_string(int32_t s) {
     default: return "unknown status";
   }
 }
+
+// Dev tooling, not declared in include/mustafar.h: per-CTA {start ns, end ns, smid} of the last
+// attention launch made with MSTF_TRACE set.
+int mstf_dev_trace(void* host, int32_t n) { return copy_trace(host, n) == cudaSuccess ? MSTF_OK : MSTF_ECUDA; }
 
 const char* mstf_build_info(void) { return "mustafar-b200 sm_100a (mma.sync m16n8k16, cp.async.bulk, mbarrier)"; }
 

@@ -49,6 +49,12 @@ struct AttnParams {
   uint32_t off_handoff;             // byte offset of the K->V mailbox (split kernel)
   uint32_t reg_k, reg_v;            // per-warp pair-array region bytes (K, V)
   int* tickets;                     // [U] arrival counters for the fused combine
+  int32_t sk;                       // 1: stream-K schedule (grid = CTAs), 0: split grid (S, U)
+  int32_t sk_q;                     // stream-K: items per CTA
+  int32_t sk_nb;                    // stream-K: items per unit if uniform, 0 = ragged (smem prefix)
+  uint32_t off_pref;                // stream-K ragged: byte offset of the prefix array in smem
+  int32_t trace;                    // dev: record per-CTA start/end/SM into g_trace
+  int32_t sk_rot;                   // dev: rotate the CTA -> item-range assignment
   void* out;
   int out_f16;
 };
@@ -108,6 +114,13 @@ __device__ __forceinline__ uint32_t lds_abs(uint32_t saddr) {
   uint32_t v;
   asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
   return v;
+}
+// Gather only when the dibit keeps a channel (mask != 0): idle lanes take no bank slot.
+__device__ __forceinline__ uint32_t lds_abs_masked(uint32_t saddr, uint32_t mask) {
+  uint32_t v = 0;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
+      : "+r"(v) : "r"(saddr), "r"(mask) : "memory");
+  return v & mask;
 }
 __device__ __forceinline__ void sts_abs(uint32_t saddr, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
@@ -336,7 +349,7 @@ __device__ __forceinline__ void gather16_s(const uint8_t* smem, uint32_t w, uint
 #define MSTF_G(J)                                                                 \
   {                                                                               \
     const uint32_t pc = __popc(w * (1u << (31 - 2 * J)));                         \
-    out[J] = lds_abs(base + STRIDE * pc) & dibit_mask<J>(cp);                      \
+    out[J] = lds_abs_masked(base + STRIDE * pc, dibit_mask<J>(cp));                \
   }
   MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
   MSTF_G(8) MSTF_G(9) MSTF_G(10) MSTF_G(11) MSTF_G(12) MSTF_G(13) MSTF_G(14) MSTF_G(15)
@@ -350,7 +363,7 @@ __device__ __forceinline__ void gather8_s(const uint8_t* smem, uint32_t hw, uint
 #define MSTF_G(J)                                                                 \
   {                                                                               \
     const uint32_t pc = __popc(hw * (1u << (31 - 2 * J)));                        \
-    out[J] = lds_abs(base + STRIDE * pc) & dibit_mask<J>(cp);                      \
+    out[J] = lds_abs_masked(base + STRIDE * pc, dibit_mask<J>(cp));                \
   }
   MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
 #undef MSTF_G
@@ -751,7 +764,7 @@ constexpr int kBarBytesKV = 256;   // full[8], empty[8], hfull[8], hempty[8]
 constexpr int kHandoffBytes = 4 * 2 * 32 * 16;
 
 template <int NK, int NV, bool INTERLEAVED>
-__global__ void __launch_bounds__(kThreadsKV, 2) mstf_attn_kv_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(kThreadsKV, 3) mstf_attn_kv_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
@@ -981,33 +994,35 @@ __global__ void __launch_bounds__(kThreadsKV, 2) mstf_attn_kv_kernel(const AttnP
 // Called by every thread of a CTA after its warps stored their partials. The last CTA of the unit
 // (ticket counter in the workspace) merges the S * 4 partials and writes the output; the ticket
 // is reset to 0 so the workspace is reusable (it must be zeroed once before first use).
-__device__ __forceinline__ void combine_if_last(const AttnParams& p, int u, int S, void* out, int out_f16) {
+
+// Fused split combine: unit u's partials are [part_begin, part_begin + nparts) and `expected`
+// CTAs arrive; the last one to take a ticket merges them. Called by every thread of the CTA.
+__device__ __forceinline__ void combine_parts_if_last(const AttnParams& p, int u, int part_begin, int nparts, int expected) {
   __shared__ int s_last;
-  __threadfence();
+  __threadfence();  // publish this CTA's partials before its ticket
   __syncthreads();
   if (threadIdx.x == 0) {
     const int prev = atomicAdd(p.tickets + u, 1);
-    s_last = (prev == S - 1);
+    s_last = (prev == expected - 1);
     if (s_last) p.tickets[u] = 0;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int nparts = S * kConsumerWarps;
   const int G = p.G;
   const int nthreads = blockDim.x;
   // one warp per head; lane owns channels 4*lane..4*lane+3
   for (int h = threadIdx.x >> 5; h < G; h += nthreads >> 5) {
     const int lane = threadIdx.x & 31;
     float M = -INFINITY;
-    for (int i = lane; i < nparts; i += 32) M = fmaxf(M, __ldcg(p.ws_ml + (((size_t)u * nparts + i) * G + h) * 2));
+    for (int i = lane; i < nparts; i += 32) M = fmaxf(M, __ldcg(p.ws_ml + (((size_t)part_begin + i) * G + h) * 2));
 #pragma unroll
     for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
     for (int i = 0; i < nparts; ++i) {
-      const size_t pi = (size_t)u * nparts + i;
+      const size_t pi = (size_t)part_begin + i;
       const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (pi * G + h) * 2));
       const float4 o = __ldcg(reinterpret_cast<const float4*>(p.ws_o + (pi * G + h) * kD + 4 * lane));
       const float wgt = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
@@ -1016,12 +1031,12 @@ __device__ __forceinline__ void combine_if_last(const AttnParams& p, int u, int 
     }
     const float inv = 1.f / L;
     const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
-    if (out_f16) {
-      __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(out) + oi);
+    if (p.out_f16) {
+      __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.out) + oi);
       po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
       po[1] = __floats2half2_rn(acc.z * inv, acc.w * inv);
     } else {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + oi) =
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oi) =
           make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     }
   }
@@ -1078,6 +1093,33 @@ __device__ __forceinline__ void store_pairs(uint8_t* smem, const RawRegs<NCH>& r
   }
 }
 
+// Work schedule. A unit's work items are its compressed 16-token blocks (ceil(n_comp/16))
+// followed by its window row blocks (ceil(W/16)). Split mode (sk == 0): grid (S, U), CTA
+// (x, u) takes the x-th of S equal item ranges of unit u; partial slot u*S + x. Stream-K mode
+// (sk == 1): grid (C), the units' item lists are concatenated and CTA c takes items
+// [c*Q, (c+1)*Q), which may cross unit boundaries; the segment (c, u) uses partial slot c + u
+// (injective: along the monotone path of (c, u) segments c + u strictly increases), and unit
+// u's partials are the slots of CTAs first(u)..last(u).
+// Dev-only CTA timeline (MSTF_TRACE=1): {start ns, end ns, smid} per CTA.
+constexpr int kTraceMax = 8192;
+__device__ unsigned long long g_trace[3 * kTraceMax];
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// Stream-K: first item of unit u (u = U gives the total). Ragged caches read the prefix array
+// the CTA built in shared memory; recomputed from the params where needed (no live registers).
+__device__ __forceinline__ int unit_start(const AttnParams& p, const uint8_t* smem, int u) {
+  return p.sk_nb ? u * p.sk_nb : reinterpret_cast<const int*>(smem + p.off_pref)[u];
+}
+
 template <int NK, int NV>
 __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1085,14 +1127,14 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
   uint64_t* hempty = hfull + 8;
   uint4* handoff = reinterpret_cast<uint4*>(smem + 128);
 
-  const int u = blockIdx.y, split = blockIdx.x, S = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CacheView& c = p.c;
-  const int n = c.n_comp[u];
-  // split the unit's 16-token blocks contiguously over the S CTAs
-  const int blocks_total = (n + 15) / 16;
-  const int bps = (blocks_total + S - 1) / S;
-  const int bbeg = min(split * bps, blocks_total), bend = min(bbeg + bps, blocks_total);
+  const int nwb = c.W > 0 ? (c.W + 15) / 16 : 0;  // window row blocks per unit
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  if (p.trace && threadIdx.x == 0 && cta < kTraceMax) {
+    g_trace[3 * cta] = global_ns();
+    g_trace[3 * cta + 2] = smid();
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < 8; ++i) {
       mbar_init(&hfull[i], 1);
@@ -1100,214 +1142,341 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
     }
     fence_mbar_init();
   }
+  if (p.sk && p.sk_nb == 0) {
+    // ragged stream-K: warp 0 scans the per-unit item counts into smem
+    int* pref = reinterpret_cast<int*>(smem + p.off_pref);
+    if (warp == 0) {
+      int carry = 0;
+      for (int u0 = 0; u0 < c.U; u0 += 32) {
+        const int uu = u0 + lane;
+        const int items = uu < c.U ? (c.n_comp[uu] + 15) / 16 + nwb : 0;
+        int incl = items;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (uu < c.U) pref[uu] = carry + incl - items;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) pref[c.U] = carry;
+    }
+  }
   __syncthreads();
+
+  // Segment bookkeeping lives in shared memory (re-read where used) so that it does not hold
+  // registers across the block loops: [0] unit, [1] first item, [2] CTA end item,
+  // [3] lo, [4] hi (unit-relative), [5] unit start, [6] unit end (absolute items).
+  __shared__ int s_seg[8];
+  const volatile int* seg = s_seg;
+  if (threadIdx.x == 0) {
+    int u0, it0, it_end0;
+    if (p.sk) {
+      it0 = ((blockIdx.x + p.sk_rot) % gridDim.x) * p.sk_q;
+      it_end0 = min(it0 + p.sk_q, unit_start(p, smem, c.U));
+      if (p.sk_nb == 0) {
+        int lo = 0, hi = c.U;  // largest u with start(u) <= it0
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (unit_start(p, smem, mid) <= it0) lo = mid; else hi = mid;
+        }
+        u0 = lo;
+      } else {
+        u0 = it0 / p.sk_nb;
+      }
+    } else {
+      u0 = blockIdx.y;
+      const int items = (c.n_comp[u0] + 15) / 16 + nwb;
+      const int per = (items + gridDim.x - 1) / gridDim.x;
+      it0 = min((int)blockIdx.x * per, items);
+      it_end0 = min(it0 + per, items);
+    }
+    s_seg[0] = u0; s_seg[1] = it0; s_seg[2] = it_end0;
+  }
 
   const bool is_k = warp < 4;
   const int w = warp & 3;
   const int g = lane >> 2, t = lane & 3;
   const uint32_t ybase = p.off_pairs + (is_k ? (uint32_t)w * p.reg_k : 4 * p.reg_k + (uint32_t)w * p.reg_v);
-  const size_t pidx = ((size_t)u * S + split) * kConsumerWarps + w;
-  const int nwin_blocks = (split == S - 1 && c.W > 0) ? (c.W + 15) / 16 : 0;
-  const int nw = c.n_win[u];
-  const int first = c.W > 0 ? n % c.W : 0;
+  int blk = 0;  // handoff sequence number (K-warp w and V-warp w+4 walk the same blocks)
+
+  // Segment prologue/epilogue shared by both roles; each role runs its own segment loop so
+  // that registers are allocated per role.
+  auto segment_begin = [&]() {
+    // ---- segment: unit u, unit-relative items [lo, hi)
+    if (threadIdx.x == 0) {
+      const int u0 = s_seg[0], it0 = s_seg[1], it_end0 = s_seg[2];
+      const int ustart = p.sk ? unit_start(p, smem, u0) : 0;
+      const int uend = p.sk ? unit_start(p, smem, u0 + 1) : it_end0;
+      s_seg[3] = it0 - ustart;
+      s_seg[4] = min(it_end0, uend) - ustart;
+      s_seg[5] = ustart;
+      s_seg[6] = uend;
+    }
+    __syncthreads();
+  };
+  auto segment_end = [&]() -> bool {
+    {
+      const int uu = seg[0];
+      if (p.sk) {
+        const int cf = seg[5] / p.sk_q, cl = (seg[6] - 1) / p.sk_q;
+        combine_parts_if_last(p, uu, (cf + uu) * kConsumerWarps, (cl - cf + 1) * kConsumerWarps, cl - cf + 1);
+      } else {
+        combine_parts_if_last(p, uu, uu * gridDim.x * kConsumerWarps, gridDim.x * kConsumerWarps, gridDim.x);
+      }
+    }
+    if (!p.sk || seg[2] <= seg[6]) return false;
+    __syncthreads();  // everyone has read this segment's bookkeeping
+    if (threadIdx.x == 0) {
+      s_seg[1] = s_seg[6];
+      s_seg[0] = s_seg[0] + 1;
+    }
+    return true;
+  };
 
   if (is_k) {
-    // ================= K-warp
-    const uint16_t* vals = c.val[0] + (size_t)u * c.cap * c.kpad[0];
-    const uint64_t* bms = c.bm[0] + (size_t)u * c.cap * kTiles;
-    KState st;
-    st.m0 = st.m1 = -INFINITY;
-    st.l0 = st.l1 = 0.f;
-    if (g < p.G) {
-      const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + g) * kD + 32 * t);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint4 x = qp[i];
-        st.qf[4 * i] = x.x; st.qf[4 * i + 1] = x.y; st.qf[4 * i + 2] = x.z; st.qf[4 * i + 3] = x.w;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) st.qf[i] = 0;
-    }
-    int blk = 0;
-    auto handoff_put = [&](const uint4 hh) {
-      const int slot = blk & 1;
-      if (blk >= 2) mbar_wait(&hempty[2 * w + slot], ((blk >> 1) - 1) & 1);
-      handoff[(w * 2 + slot) * 32 + lane] = hh;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&hfull[2 * w + slot]);
-      ++blk;
-    };
-    auto k_step = [&](const RawRegs<NK>& cur, int b) {
-      const int nvalid = min(16, n - b * 16);
-      __syncwarp();
-      store_pairs<NK, false>(smem, cur, ybase, lane);
-      const uint32_t pk = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
-      uint32_t ik = pk;
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
-        if (t >= o) ik += y;
-      }
-      const uint32_t ek = ik - pk;
-      __syncwarp();
-      uint32_t kr[2][16];
-      gather16_s<32>(smem, cur.bm0, ybase + 4u * (uint32_t)(KLayout<NK>::k0 + g) + 32u * (ek & 0xFFFF), kr[0]);
-      gather16_s<32>(smem, cur.bm1, ybase + 4u * (uint32_t)(KLayout<NK>::k1 + g) + 32u * (ek >> 16), kr[1]);
-      handoff_put(k_block(kr, g < nvalid, g + 8 < nvalid, st, p.scale_log2));
-    };
-    {
-      RawRegs<NK> ra, rb;
-      int b = bbeg + w;
-      if (b < bend) load_raw<NK>(ra, vals, bms, b * 16, min(16, n - b * 16), lane);
-      while (b < bend) {
-        if (b + 4 < bend) load_raw<NK>(rb, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
-        k_step(ra, b);
-        b += 4;
-        if (b >= bend) break;
-        if (b + 4 < bend) load_raw<NK>(ra, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
-        k_step(rb, b);
-        b += 4;
-      }
-    }
-    for (int blkw = w; blkw < nwin_blocks; blkw += 4) {
-      DenseBlock db;
-      db.k = c.win[0] + (size_t)u * c.W * kD;
-      db.v = c.win[1] + (size_t)u * c.W * kD;
-      db.ring = true; db.row0 = blkw * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
-      bool any = false;
-#pragma unroll
-      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
-      if (!any) continue;
-      uint32_t kr[2][16];
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const int tok = g + 8 * x;
-        if (db.valid(tok)) {
-          const uint4* pp = reinterpret_cast<const uint4*>(db.k + (size_t)(db.row0 + tok) * kD + 32 * t);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint4 a = pp[j];
-            kr[x][4 * j] = a.x; kr[x][4 * j + 1] = a.y; kr[x][4 * j + 2] = a.z; kr[x][4 * j + 3] = a.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) kr[x][j] = 0;
-        }
-      }
-      handoff_put(k_block(kr, db.valid(g), db.valid(g + 8), st, p.scale_log2));
-    }
-    float l0 = st.l0, l1 = st.l1;
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-    }
-    float* ml = p.ws_ml + pidx * p.G * 2;
-    if (g == 0) {
-      if (2 * t < p.G) { ml[4 * t] = st.m0; ml[4 * t + 1] = l0; }
-      if (2 * t + 1 < p.G) { ml[4 * t + 2] = st.m1; ml[4 * t + 3] = l1; }
-    }
-  } else {
-    // ================= V-warp
-    const uint16_t* vals = c.val[1] + (size_t)u * c.cap * c.kpad[1];
-    const uint64_t* bms = c.bm[1] + (size_t)u * c.cap * kTiles;
-    float acc[2][4][4];
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[e][i][0] = acc[e][i][1] = acc[e][i][2] = acc[e][i][3] = 0.f;
-    int blk = 0;
-    auto handoff_get = [&]() -> uint4 {
-      const int slot = blk & 1;
-      mbar_wait(&hfull[2 * w + slot], (blk >> 1) & 1);
-      const uint4 hh = handoff[(w * 2 + slot) * 32 + lane];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&hempty[2 * w + slot]);
-      ++blk;
-      return hh;
-    };
-    auto v_step = [&](const RawRegs<NV>& cur) {
-      __syncwarp();
-      store_pairs<NV, true>(smem, cur, ybase, lane);
-      const uint32_t pv = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
-      uint32_t iv = pv;
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o, 4);
-        if (t >= o) iv += y;
-      }
-      const uint32_t ev = iv - pv;
-      __syncwarp();
-      const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
-      const uint32_t w2t = __shfl_sync(0xffffffffu, cur.bm0, sa), w2t8 = __shfl_sync(0xffffffffu, cur.bm1, sa);
-      const uint32_t w2t1 = __shfl_sync(0xffffffffu, cur.bm0, sb), w2t9 = __shfl_sync(0xffffffffu, cur.bm1, sb);
-      const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
-      const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
-      const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
-      uint32_t vr[4][8];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
-        const uint32_t base = ybase + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * (ps[x] + extra);
-        gather8_s<16>(smem, ws[x] >> hsh, base, vr[x]);
-      }
-      v_block(vr, handoff_get(), acc);
-    };
-    {
-      RawRegs<NV> ra, rb;
-      int b = bbeg + w;
-      if (b < bend) load_raw<NV>(ra, vals, bms, b * 16, min(16, n - b * 16), lane);
-      while (b < bend) {
-        if (b + 4 < bend) load_raw<NV>(rb, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
-        v_step(ra);
-        b += 4;
-        if (b >= bend) break;
-        if (b + 4 < bend) load_raw<NV>(ra, vals, bms, (b + 4) * 16, min(16, n - (b + 4) * 16), lane);
-        v_step(rb);
-        b += 4;
-      }
-    }
-    for (int blkw = w; blkw < nwin_blocks; blkw += 4) {
-      DenseBlock db;
-      db.k = c.win[0] + (size_t)u * c.W * kD;
-      db.v = c.win[1] + (size_t)u * c.W * kD;
-      db.ring = true; db.row0 = blkw * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
-      bool any = false;
-#pragma unroll
-      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
-      if (!any) continue;
-      uint32_t vr[4][8];
-      const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        if (db.valid(tk[x])) {
-          const uint4* pp = reinterpret_cast<const uint4*>(db.v + (size_t)(db.row0 + tk[x]) * kD + 16 * g);
-          const uint4 a = pp[0], bb = pp[1];
-          vr[x][0] = a.x; vr[x][1] = a.y; vr[x][2] = a.z; vr[x][3] = a.w;
-          vr[x][4] = bb.x; vr[x][5] = bb.y; vr[x][6] = bb.z; vr[x][7] = bb.w;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) vr[x][j] = 0;
-        }
-      }
-      v_block(vr, handoff_get(), acc);
-    }
-    float* o = p.ws_o + pidx * p.G * kD;
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int h = 2 * t + hh;
-      if (h < p.G) {
+    for (;;) {
+      segment_begin();
+      const int u = seg[0];
+      const int n = c.n_comp[u];
+      const int nbc = (n + 15) / 16;
+      const int bbeg = min((int)seg[3], nbc), bend = min((int)seg[4], nbc);
+      // window items x in [max(lo, nbc), hi) go to warp (x - lo) % 4 (computed after the main loop)
+      auto first_window_item = [&]() {
+        const int lo = seg[3];
+        const int xw0 = max(lo, nbc);
+        return xw0 + ((w - (xw0 - lo)) % 4 + 4) % 4;
+      };
+      auto part_index = [&]() -> size_t {
+        const int uu = seg[0];
+        const int slot = p.sk ? (int)((blockIdx.x + p.sk_rot) % gridDim.x) + uu : uu * (int)gridDim.x + (int)blockIdx.x;
+        return (size_t)slot * kConsumerWarps + w;
+      };
+
+      // ================= K-warp
+      KState st;
+      st.m0 = st.m1 = -INFINITY;
+      st.l0 = st.l1 = 0.f;
+      if (g < p.G) {
+        const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + g) * kD + 32 * t);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          *reinterpret_cast<float2*>(o + h * kD + 16 * g + 2 * i) = make_float2(acc[0][i][hh], acc[1][i][hh]);
-          *reinterpret_cast<float2*>(o + h * kD + 16 * g + 8 + 2 * i) =
-              make_float2(acc[0][i][2 + hh], acc[1][i][2 + hh]);
+          const uint4 x = qp[i];
+          st.qf[4 * i] = x.x; st.qf[4 * i + 1] = x.y; st.qf[4 * i + 2] = x.z; st.qf[4 * i + 3] = x.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) st.qf[i] = 0;
+      }
+      auto handoff_put = [&](const uint4 hh) {
+        const int hs = blk & 1;
+        if (blk >= 2) mbar_wait(&hempty[2 * w + hs], ((blk >> 1) - 1) & 1);
+        handoff[(w * 2 + hs) * 32 + lane] = hh;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hfull[2 * w + hs]);
+        ++blk;
+      };
+      auto k_step = [&](const RawRegs<NK>& cur, int b) {
+        const int nvalid = min(16, n - b * 16);
+        __syncwarp();
+        store_pairs<NK, false>(smem, cur, ybase, lane);
+        const uint32_t pk = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
+        uint32_t ik = pk;
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
+          if (t >= o) ik += y;
+        }
+        const uint32_t ek = ik - pk;
+        __syncwarp();
+        uint32_t kr[2][16];
+        gather16_s<32>(smem, cur.bm0, ybase + 4u * (uint32_t)(KLayout<NK>::k0 + g) + 32u * (ek & 0xFFFF), kr[0]);
+        gather16_s<32>(smem, cur.bm1, ybase + 4u * (uint32_t)(KLayout<NK>::k1 + g) + 32u * (ek >> 16), kr[1]);
+        handoff_put(k_block(kr, g < nvalid, g + 8 < nvalid, st, p.scale_log2));
+      };
+      {
+        // unit base pointers are re-derived per load (seg[0], params) to save registers
+        auto load = [&](RawRegs<NK>& rr, int bb) {
+          const size_t ub = (size_t)seg[0] * c.cap;
+          load_raw<NK>(rr, c.val[0] + ub * c.kpad[0], c.bm[0] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
+        };
+        RawRegs<NK> ra, rb;
+        int b = bbeg + w;
+        if (b < bend) load(ra, b);
+        while (b < bend) {
+          if (b + 4 < bend) load(rb, b + 4);
+          k_step(ra, b);
+          b += 4;
+          if (b >= bend) break;
+          if (b + 4 < bend) load(ra, b + 4);
+          k_step(rb, b);
+          b += 4;
         }
       }
+      const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
+      for (int x = first_window_item(), hi = seg[4]; x < hi; x += 4) {
+        DenseBlock db;
+        db.k = c.win[0] + (size_t)u * c.W * kD;
+        db.v = c.win[1] + (size_t)u * c.W * kD;
+        db.ring = true; db.row0 = (x - nbc) * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
+        bool any = false;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
+        if (!any) continue;
+        uint32_t kr[2][16];
+#pragma unroll
+        for (int xx = 0; xx < 2; ++xx) {
+          const int tok = g + 8 * xx;
+          if (db.valid(tok)) {
+            const uint4* pp = reinterpret_cast<const uint4*>(db.k + (size_t)(db.row0 + tok) * kD + 32 * t);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 a4 = pp[j];
+              kr[xx][4 * j] = a4.x; kr[xx][4 * j + 1] = a4.y; kr[xx][4 * j + 2] = a4.z; kr[xx][4 * j + 3] = a4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) kr[xx][j] = 0;
+          }
+        }
+        handoff_put(k_block(kr, db.valid(g), db.valid(g + 8), st, p.scale_log2));
+      }
+      float l0 = st.l0, l1 = st.l1;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      }
+      float* ml = p.ws_ml + part_index() * p.G * 2;
+      if (g == 0) {
+        if (2 * t < p.G) { ml[4 * t] = st.m0; ml[4 * t + 1] = l0; }
+        if (2 * t + 1 < p.G) { ml[4 * t + 2] = st.m1; ml[4 * t + 3] = l1; }
+      }
+      if (!segment_end()) break;
+    }
+    if (p.trace && threadIdx.x == 0 && cta < kTraceMax) g_trace[3 * cta + 1] = global_ns();
+  } else {
+    for (;;) {
+      segment_begin();
+      const int u = seg[0];
+      const int n = c.n_comp[u];
+      const int nbc = (n + 15) / 16;
+      const int bbeg = min((int)seg[3], nbc), bend = min((int)seg[4], nbc);
+      // window items x in [max(lo, nbc), hi) go to warp (x - lo) % 4 (computed after the main loop)
+      auto first_window_item = [&]() {
+        const int lo = seg[3];
+        const int xw0 = max(lo, nbc);
+        return xw0 + ((w - (xw0 - lo)) % 4 + 4) % 4;
+      };
+      auto part_index = [&]() -> size_t {
+        const int uu = seg[0];
+        const int slot = p.sk ? (int)((blockIdx.x + p.sk_rot) % gridDim.x) + uu : uu * (int)gridDim.x + (int)blockIdx.x;
+        return (size_t)slot * kConsumerWarps + w;
+      };
+
+      // ================= V-warp
+      float acc[2][4][4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[e][i][0] = acc[e][i][1] = acc[e][i][2] = acc[e][i][3] = 0.f;
+      auto handoff_get = [&]() -> uint4 {
+        const int hs = blk & 1;
+        mbar_wait(&hfull[2 * w + hs], (blk >> 1) & 1);
+        const uint4 hh = handoff[(w * 2 + hs) * 32 + lane];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hempty[2 * w + hs]);
+        ++blk;
+        return hh;
+      };
+      auto v_step = [&](const RawRegs<NV>& cur) {
+        __syncwarp();
+        store_pairs<NV, true>(smem, cur, ybase, lane);
+        const uint32_t pv = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
+        uint32_t iv = pv;
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o, 4);
+          if (t >= o) iv += y;
+        }
+        const uint32_t ev = iv - pv;
+        __syncwarp();
+        const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
+        const uint32_t w2t = __shfl_sync(0xffffffffu, cur.bm0, sa), w2t8 = __shfl_sync(0xffffffffu, cur.bm1, sa);
+        const uint32_t w2t1 = __shfl_sync(0xffffffffu, cur.bm0, sb), w2t9 = __shfl_sync(0xffffffffu, cur.bm1, sb);
+        const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
+        const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
+        const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
+        uint32_t vr[4][8];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
+          const uint32_t base = ybase + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * (ps[x] + extra);
+          gather8_s<16>(smem, ws[x] >> hsh, base, vr[x]);
+        }
+        v_block(vr, handoff_get(), acc);
+      };
+      {
+        // unit base pointers are re-derived per load (seg[0], params) to save registers
+        auto load = [&](RawRegs<NV>& rr, int bb) {
+          const size_t ub = (size_t)seg[0] * c.cap;
+          load_raw<NV>(rr, c.val[1] + ub * c.kpad[1], c.bm[1] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
+        };
+        RawRegs<NV> ra, rb;
+        int b = bbeg + w;
+        if (b < bend) load(ra, b);
+        while (b < bend) {
+          if (b + 4 < bend) load(rb, b + 4);
+          v_step(ra);
+          b += 4;
+          if (b >= bend) break;
+          if (b + 4 < bend) load(ra, b + 4);
+          v_step(rb);
+          b += 4;
+        }
+      }
+      const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
+      for (int x = first_window_item(), hi = seg[4]; x < hi; x += 4) {
+        DenseBlock db;
+        db.k = c.win[0] + (size_t)u * c.W * kD;
+        db.v = c.win[1] + (size_t)u * c.W * kD;
+        db.ring = true; db.row0 = (x - nbc) * 16; db.nvalid = 0; db.W = c.W; db.first = first; db.nwin = nw;
+        bool any = false;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
+        if (!any) continue;
+        uint32_t vr[4][8];
+        const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
+#pragma unroll
+        for (int x4 = 0; x4 < 4; ++x4) {
+          if (db.valid(tk[x4])) {
+            const uint4* pp = reinterpret_cast<const uint4*>(db.v + (size_t)(db.row0 + tk[x4]) * kD + 16 * g);
+            const uint4 a4 = pp[0], bb = pp[1];
+            vr[x4][0] = a4.x; vr[x4][1] = a4.y; vr[x4][2] = a4.z; vr[x4][3] = a4.w;
+            vr[x4][4] = bb.x; vr[x4][5] = bb.y; vr[x4][6] = bb.z; vr[x4][7] = bb.w;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) vr[x4][j] = 0;
+          }
+        }
+        v_block(vr, handoff_get(), acc);
+      }
+      float* o = p.ws_o + part_index() * p.G * kD;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int h = 2 * t + hh;
+        if (h < p.G) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            *reinterpret_cast<float2*>(o + h * kD + 16 * g + 2 * i) = make_float2(acc[0][i][hh], acc[1][i][hh]);
+            *reinterpret_cast<float2*>(o + h * kD + 16 * g + 8 + 2 * i) =
+                make_float2(acc[0][i][2 + hh], acc[1][i][2 + hh]);
+          }
+        }
+      }
+      if (!segment_end()) break;
     }
   }
-  combine_if_last(p, u, S, p.out, p.out_f16);
 }
 
 // ---------------------------------------------------------------- K3: combine partials
@@ -1382,7 +1551,10 @@ int32_t max_splits_for(int32_t U, int32_t capacity) {
 static size_t ticket_bytes(int32_t U) { return ((size_t)U * sizeof(int) + 255) / 256 * 256; }
 
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits) {
-  const size_t parts = (size_t)U * max_splits * kConsumerWarps;
+  // split mode uses U*S partial slots, stream-K at most grid + U (grid <= kMaxSkGrid)
+  size_t slots = (size_t)U * max_splits;
+  if (slots < (size_t)U + kMaxSkGrid) slots = (size_t)U + kMaxSkGrid;
+  const size_t parts = slots * kConsumerWarps;
   return ticket_bytes(U) + parts * G * (kD + 2) * sizeof(float) + 256;
 }
 
@@ -1406,7 +1578,8 @@ static int32_t pair_region_bytes(int32_t kp, bool v) {
   return (b + 127) / 128 * 128;
 }
 
-AttnPlan plan_attention(int32_t U, int32_t max_comp, int32_t kpad_k, int32_t kpad_v, int32_t sm_count) {
+AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_t uniform_items,
+                        int32_t kpad_k, int32_t kpad_v, int32_t sm_count) {
   AttnPlan pl;
   pl.stage_bytes = kChunk * (16 + 2 * kpad_k + 16 + 2 * kpad_v);
   pl.reg_k = pair_region_bytes(kpad_k, false);
@@ -1429,6 +1602,25 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int32_t kpad_k, int32_t kpa
     if (t < best_t - 1e-9) { best_t = t; best = s; }
   }
   pl.splits = best;
+  // Stream-K schedule for the register-staged kernel: one wave of 2 CTAs per SM with equal item
+  // counts (no idle SMs in a partial wave, one prologue/epilogue per CTA). Ragged units need a
+  // (U+1)-int prefix array in shared memory; very large U keeps the split grid.
+  pl.sk = 0;
+  pl.sk_q = pl.sk_nb = pl.sk_grid = 0;
+  const int32_t nk = kpad_k / 8;
+  const bool reg_kernel = kpad_k == kpad_v && (nk == 2 || nk == 4 || nk == 5);
+  if (reg_kernel && total_items > 0 && total_items < (1ll << 30) && (uniform_items > 0 || U <= kMaxSkPrefix)) {
+    int64_t grid = 2 * (int64_t)sm_count;
+    if (grid > kMaxSkGrid) grid = kMaxSkGrid;
+    const int64_t min_q = 8;  // >= 2 blocks per warp to amortise the prologue
+    if (grid > (total_items + min_q - 1) / min_q) grid = (total_items + min_q - 1) / min_q;
+    if (grid < 1) grid = 1;
+    const int64_t q = (total_items + grid - 1) / grid;
+    pl.sk = 1;
+    pl.sk_q = (int32_t)q;
+    pl.sk_grid = (int32_t)((total_items + q - 1) / q);
+    pl.sk_nb = uniform_items;
+  }
   return pl;
 }
 
@@ -1448,12 +1640,19 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.off_handoff = p.off_pairs + plan.pair_bytes;
   p.reg_k = plan.reg_k;
   p.reg_v = plan.reg_v;
-  const size_t parts = (size_t)c.U * plan.splits * kConsumerWarps;
+  // partial slots: U*S (split grid) or grid + U (stream-K, see UnitSched)
+  const size_t parts = (plan.sk ? (size_t)c.U + plan.sk_grid : (size_t)c.U * plan.splits) * kConsumerWarps;
   p.tickets = reinterpret_cast<int*>(ws);  // [U] ticket counters at a fixed place (zero between calls)
   p.ws_o = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ticket_bytes(c.U));
   p.ws_ml = p.ws_o + parts * G * kD;
   p.out = out;
   p.out_f16 = out_f16;
+  p.sk = 0;
+  p.sk_q = p.sk_nb = 0;
+  p.off_pref = 0;
+  p.trace = std::getenv("MSTF_TRACE") != nullptr;  // dev timeline (tools/trace_ctas.py)
+  p.sk_rot = 0;
+  if (const char* e = std::getenv("MSTF_SKROT")) p.sk_rot = std::atoi(e);
   const int smem = kBarBytesKV + plan.nstage * plan.stage_bytes + plan.pair_bytes + kHandoffBytes;
   // kernel choice: register-staged interleaved kernel for kpad <= 40 (nk <= 5); TMA-staged kernel
   // with contiguous pair arrays for kpad >= 48 (interleaving aliases banks at ~50% density).
@@ -1461,13 +1660,13 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   const int nk = c.kpad[0] / 8, nv = c.kpad[1] / 8;
   if (nk == nv) {
     switch (nk) {
+      case 5: kern = mstf_attn_kv_kernel<5, 5, true>; break;
       case 8: kern = mstf_attn_kv_kernel<8, 8, false>; break;
       case 16: kern = mstf_attn_kv_kernel<16, 16, false>; break;
       default: break;
     }
   }
-  const char* kv = std::getenv("MSTF_KERNEL");
-  const bool use_reg = (nk == nv) && (nk == 2 || nk == 4 || nk == 5) && !(kv && kv[0] == 't');
+  const bool use_reg = (nk == nv) && (nk == 2 || nk == 4 || nk == 5);
   if (use_reg) {
     void (*rk)(AttnParams) = nullptr;
     switch (nk) {
@@ -1477,10 +1676,19 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
     }
     AttnParams pr = p;
     pr.off_pairs = 128 + kHandoffBytes;
-    const int rsmem = pr.off_pairs + plan.pair_bytes;
+    int rsmem = pr.off_pairs + plan.pair_bytes;
+    dim3 grid(plan.splits, c.U);
+    if (plan.sk) {
+      pr.sk = 1;
+      pr.sk_q = plan.sk_q;
+      pr.sk_nb = plan.sk_nb;
+      pr.off_pref = (uint32_t)rsmem;
+      if (plan.sk_nb == 0) rsmem += (c.U + 1) * (int)sizeof(int);
+      grid = dim3(plan.sk_grid, 1);
+    }
     cudaError_t e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
     if (e != cudaSuccess) return e;
-    rk<<<dim3(plan.splits, c.U), 256, rsmem, s>>>(pr);
+    rk<<<grid, 256, rsmem, s>>>(pr);
     return cudaGetLastError();
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1504,6 +1712,11 @@ cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const i
   if (e != cudaSuccess) return e;
   mstf_combine_kernel<<<U, G * 32, 0, s>>>(ws_o, ws_ml, splits * kConsumerWarps, G, out, out_f16);
   return cudaGetLastError();
+}
+
+cudaError_t copy_trace(void* host, int n) {
+  if (n > 3 * kTraceMax) n = 3 * kTraceMax;
+  return cudaMemcpyFromSymbol(host, g_trace, n * sizeof(unsigned long long));
 }
 
 }  // namespace mstf

@@ -11,6 +11,8 @@ constexpr int kTiles = kD / 64;  // 64-bit bitmap words per token record
 constexpr int kChunk = 64;       // tokens per TMA stage
 constexpr int kConsumerWarps = 4;
 constexpr int kMaxGroup = 8;     // query heads per unit (mma N = 8)
+constexpr int kMaxSkGrid = 2 * 148;  // stream-K grid cap (2 CTAs per SM on a B200)
+constexpr int kMaxSkPrefix = 16384;  // ragged stream-K: max units (prefix array in smem)
 
 // Device view of one cache (one tensor = K or V shares the same layout).
 struct CacheView {
@@ -37,8 +39,15 @@ struct AttnPlan {
   int32_t stage_bytes;   // bytes of one stage (K bm, K vals, V bm, V vals for kChunk tokens)
   int32_t pair_bytes;    // per-CTA shifted pair arrays (4 warps x 16 tokens x K,V)
   int32_t reg_k, reg_v;  // per-warp region bytes
+  int32_t sk;            // 1: stream-K schedule (register-staged kernel)
+  int32_t sk_q;          // items (16-token blocks) per CTA
+  int32_t sk_nb;         // items per unit when all units are equal, else 0
+  int32_t sk_grid;       // CTAs
 };
-AttnPlan plan_attention(int32_t U, int32_t max_comp, int32_t kpad_k, int32_t kpad_v, int32_t sm_count);
+// total_items = sum over units of ceil(n_comp/16) + ceil(W/16); uniform_items = that per-unit count
+// when it is the same for every unit, else 0.
+AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_t uniform_items,
+                        int32_t kpad_k, int32_t kpad_v, int32_t sm_count);
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits);
 int32_t max_splits_for(int32_t U, int32_t capacity);
 
@@ -48,5 +57,8 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
 cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const int32_t* lengths, int32_t U,
                                    int32_t G, int32_t t_max, int32_t splits, const uint16_t* q, float scale,
                                    void* out, int32_t out_f16, void* ws, cudaStream_t s);
+
+// dev: copy the per-CTA timeline recorded when MSTF_TRACE is set (n = 3 * CTAs words)
+cudaError_t copy_trace(void* host, int n);
 
 }  // namespace mstf

@@ -169,6 +169,25 @@ def test_attention_ragged_units(M):
     assert check_attention(M, gc, oc, 2, 16, 4, seed=77) <= TOL
 
 
+@pytest.mark.parametrize("sched", ["split", "stream-k"])
+@pytest.mark.parametrize("case", [
+    # (batch, hq, hkv, T, keep, W, lengths per unit or None)
+    (16, 32, 8, 600, 39, 32, None),                                   # uniform: stream-K without prefix
+    (3, 8, 2, 777, 39, 0, [777, 5, 300, 1, 64, 65]),                  # ragged, no window
+    (64, 8, 2, 300, 39, 32, [(37 * i) % 300 + 1 for i in range(128)]),  # ragged, many units
+    (2, 8, 2, 1000, 32, 32, [1000, 17, 16, 999]),                     # kpad 32 kernel
+    (2, 8, 2, 1000, 16, 16, None),                                    # kpad 16 kernel
+])
+def test_attention_schedules(M, monkeypatch, sched, case):
+    """Both work schedules of the register-staged kernel (split grid; stream-K with units
+    concatenated and CTA ranges crossing unit boundaries) against the oracle."""
+    U_b, hq, hkv, T, keep, W, lengths = case
+    if sched == "split":
+        monkeypatch.setenv("MSTF_SCHED", "split")
+    gc, oc = make(M, U_b, hq, hkv, T, keep, keep, W, lengths=lengths, seed=T + keep)
+    assert check_attention(M, gc, oc, U_b, hq, hkv, seed=T) <= TOL
+
+
 def test_attention_after_appends(M):
     U_b, hq, hkv, T, n = 1, 8, 2, 500, 40
     U = U_b * hkv
