@@ -1,21 +1,33 @@
-// attention.cu -- K2/K3: split-sequence decode attention directly over the compressed
-// cache (Algorithm 1), and the dense-KV baseline on the same skeleton.
+// attention.cu -- K2/K3: decode attention directly over the compressed cache
+// (Algorithm 1), and the dense-KV baseline on the same skeleton.
 //
-// K2 (mstf_attn_kernel), grid = (splits, U), block = 4 consumer warps + 1 producer warp.
-//   * producer (one lane): streams the split's compressed records chunk by chunk
-//     (kChunk tokens: K bitmaps, K values, V bitmaps, V values -- four contiguous
-//     cp.async.bulk copies) into an nstage-deep shared-memory ring guarded by mbarriers
-//     (full: tx-count, empty: one arrive per consumer warp).
-//   * consumer warp w takes tokens [16w, 16w+16) of every chunk:
-//       a5  S^T[16 tok x 8 heads] = K_blk[16 x 128] . q^T   -- 8 x mma.m16n8k16; the A
-//           operand is the K block expanded from (bitmap, packed values) in registers
-//           ("load-as-compressed, compute-as-dense"), zeros at pruned channels
-//       a7  online softmax (running max m, sum l per head, exp2 with log2e folded in)
-//       a8  O^T[128 ch x 8 heads] += V_blk^T[128 x 16] . P^T[16 x 8]  -- 8 x mma; P^T is
-//           the score accumulator converted to fp16 and transposed with movmatrix
-//     the last split also covers the dense local window (a6, Alg. 1 lines 1 and 5).
-//   * each warp writes its (m, l, o) partial to the workspace.
-// K3 (mstf_combine_kernel): per (unit, head, channel), merges the partials (a9).
+// Work item = one 16-token block of one unit (compressed records, or rows of the dense
+// window ring). Every kernel below runs K/V warp-specialised pairs: K-warp w expands a
+// block of K records into mma fragments, computes S^T[16 tok x 8 heads] = K_blk . q^T
+// (a5/a6, 8 x mma.m16n8k16, fp32 accumulate), runs the online softmax (a7, exp2 with
+// log2e folded into the scale) and hands {P^T fp16 fragments, rescale factors} through a
+// 2-slot shared-memory mailbox (mbarriers hfull/hempty) to V-warp w, which expands the
+// same block of V records and accumulates O^T[128 ch x 8 heads] += V_blk^T . P^T (a8).
+// "Load as compressed, compute as dense": the expansion writes zeros at pruned
+// channels in registers; nothing dense ever touches HBM.
+//
+// Expansion ("gather"): a warp writes each token's packed values into a shifted pair
+// array Y[m] = (h[m-1], h[m]) in shared memory; channel pair (2j, 2j+1) of bitmap word w
+// is then ONE 32-bit load at Y[popc(w & bits <= 2j)] masked by the two bitmap bits
+// (prmt sign-replicate masks), so a lane builds its fragments without branches.
+//
+// Kernels
+//   mstf_attn_reg_kernel<NK,NV>   (kpad 16/32/40; the 70%-sparsity path) 8 warps, each
+//       warp streams its blocks' records straight into registers with a one-block
+//       software pipeline, builds the pair arrays from registers, gathers, mma. Work
+//       schedule: stream-K (units' blocks concatenated, equal ranges over one wave of
+//       2 CTAs per SM; see UnitSched below) or split grid (S, U). The last CTA to finish
+//       a unit merges its partials (a9) in the same launch.
+//   mstf_attn_kv_kernel<NK,NV,I>  (other kpad, e.g. 64 at 50% sparsity) 8 consumer warps +
+//       1 producer warp streaming 64-token chunks (K bitmaps, K values, V bitmaps,
+//       V values: four cp.async.bulk copies) into an mbarrier-guarded smem ring; split grid.
+//   mstf_combine_kernel           merges the kv kernel's split partials (a9).
+//   mstf_dense_attn_kernel        dense-KV baseline (same mma/softmax code, no expansion).
 //
 // Fragment <-> channel mapping (free permutations of the contraction / output index):
 //   K mma, lane (g = lane/4, t = lane%4): tokens g and g+8, channels 32t..32t+31
@@ -32,9 +44,6 @@
 
 namespace mstf {
 
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kBarBytes = 128;  // 8 stages x {full, empty} x 8 B
-constexpr int kBarBytesHost = kBarBytes;
 
 struct AttnParams {
   CacheView c;
@@ -639,120 +648,6 @@ __device__ __forceinline__ void store_partial(WarpState& st, float* ws_o, float*
   }
 }
 
-// ---------------------------------------------------------------- K2: sparse attention
-template <int NK, int NV>
-__global__ void __launch_bounds__(kThreads, 2) mstf_attn_kernel(const AttnParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + 8;
-  uint8_t* stages = smem + kBarBytes;
-
-  const int u = blockIdx.y, split = blockIdx.x, S = gridDim.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const CacheView& c = p.c;
-  const int n = c.n_comp[u];
-  const int chunks_total = (n + kChunk - 1) / kChunk;
-  const int cps = (chunks_total + S - 1) / S;
-  const int cbeg = min(split * cps, chunks_total), cend = min(cbeg + cps, chunks_total);
-  const int nchunks = cend - cbeg;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < p.nstage; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp == kConsumerWarps) {
-    // ---------------- producer
-    if (lane == 0) {
-      const int kpk = c.kpad[0], kpv = c.kpad[1];
-      const uint8_t* kbm = reinterpret_cast<const uint8_t*>(c.bm[0] + (size_t)u * c.cap * kTiles);
-      const uint8_t* vbm = reinterpret_cast<const uint8_t*>(c.bm[1] + (size_t)u * c.cap * kTiles);
-      const uint8_t* kval = reinterpret_cast<const uint8_t*>(c.val[0] + (size_t)u * c.cap * kpk);
-      const uint8_t* vval = reinterpret_cast<const uint8_t*>(c.val[1] + (size_t)u * c.cap * kpv);
-      for (int i = 0; i < nchunks; ++i) {
-        const int st = i % p.nstage;
-        if (i >= p.nstage) mbar_wait(&empty[st], ((i / p.nstage) - 1) & 1);
-        const int tok0 = (cbeg + i) * kChunk;
-        const int nt = min(kChunk, n - tok0);
-        const uint32_t bbm = nt * 16, bk = nt * 2 * kpk, bv = nt * 2 * kpv;
-        uint8_t* sb = stages + (size_t)st * p.stage_bytes;
-        mbar_arrive_expect_tx(&full[st], 2 * bbm + bk + bv);
-        bulk_g2s(sb, kbm + (size_t)tok0 * 16, bbm, &full[st]);
-        bulk_g2s(sb + p.off_kval, kval + (size_t)tok0 * 2 * kpk, bk, &full[st]);
-        bulk_g2s(sb + p.off_vbm, vbm + (size_t)tok0 * 16, bbm, &full[st]);
-        bulk_g2s(sb + p.off_vval, vval + (size_t)tok0 * 2 * kpv, bv, &full[st]);
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers
-  WarpState st;
-  init_state(st, p.q + (size_t)u * p.G * kD, p.G, lane);
-  const int g = lane >> 2;
-  CompBlock cb;
-  cb.smem = smem;
-  cb.kpk = c.kpad[0];
-  cb.kpv = c.kpad[1];
-  cb.strk = 4 * cb.kpk + 16;
-  cb.strv = 4 * cb.kpv + 16;
-  cb.yk = p.off_pairs + (uint32_t)warp * 16 * (cb.strk + cb.strv);
-  cb.yv = cb.yk + 16 * cb.strk;
-  cb.tok0 = 16 * warp;
-  for (int i = 0; i < nchunks; ++i) {
-    const int sidx = i % p.nstage;
-    mbar_wait(&full[sidx], (i / p.nstage) & 1);
-    const uint32_t sb = kBarBytes + (uint32_t)sidx * p.stage_bytes;
-    const int tok0 = (cbeg + i) * kChunk;
-    const int nvalid = min(16, n - tok0 - 16 * warp);
-    if (nvalid > 0) {
-      cb.kbm = sb;
-      cb.kval = sb + p.off_kval;
-      cb.vbm = sb + p.off_vbm;
-      cb.vval = sb + p.off_vval;
-      cb.nvalid = nvalid;
-      BlockRegs r;
-      fill_compressed<NK, NV>(cb, smem, r, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[sidx]);
-      process_block(r, g < nvalid, g + 8 < nvalid, st, p.scale_log2);
-    } else {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[sidx]);
-    }
-  }
-  // dense local window (Alg. 1 lines 1 and 5) on the last split
-  if (split == S - 1 && c.W > 0) {
-    const int nw = c.n_win[u];
-    const int first = n % c.W;  // slot of the oldest window token (position n)
-    for (int blk = warp; blk * 16 < c.W; blk += kConsumerWarps) {
-      DenseBlock db;
-      db.k = c.win[0] + (size_t)u * c.W * kD;
-      db.v = c.win[1] + (size_t)u * c.W * kD;
-      db.ring = true;
-      db.row0 = blk * 16;
-      db.nvalid = 0;
-      db.W = c.W;
-      db.first = first;
-      db.nwin = nw;
-      bool any = false;
-#pragma unroll
-      for (int rr = 0; rr < 16; ++rr) any |= db.valid(rr);
-      if (any) {
-        BlockRegs r;
-        fill_dense(db, r, lane);
-        process_block(r, db.valid(g), db.valid(g + 8), st, p.scale_log2);
-      }
-    }
-  }
-  const size_t pidx = ((size_t)u * S + split) * kConsumerWarps + warp;
-  store_partial(st, p.ws_o, p.ws_ml, pidx, p.G, lane);
-}
-
 // ---------------------------------------------------------------- K2 (K/V warp-specialised)
 // 4 K-warps (0..3) + 4 V-warps (4..7) + 1 producer warp (8). K-warp w and V-warp w+4 share the
 // tokens [16w, 16w+16) of every stage: the K-warp gathers K, computes scores and the online
@@ -764,7 +659,7 @@ constexpr int kBarBytesKV = 256;   // full[8], empty[8], hfull[8], hempty[8]
 constexpr int kHandoffBytes = 4 * 2 * 32 * 16;
 
 template <int NK, int NV, bool INTERLEAVED>
-__global__ void __launch_bounds__(kThreadsKV, 3) mstf_attn_kv_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(kThreadsKV, 2) mstf_attn_kv_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 8;
