@@ -348,7 +348,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
                 "h2d_bytes_per_step": per_step_in, "d2h_bytes_per_step": U * G * d * 2,
                 "steps": e2e_steps, "ms_per_step": round(e2e_ms, 4)},
-        "gpu_launches": K_steps * L * 3,
+        "gpu_launches": K_steps * L * (1 + caches[0].attention_kernel_count()),  # append + attention
         "clocks": clocks,
         "dense_kv": dense,
     }

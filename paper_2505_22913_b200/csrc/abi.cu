@@ -243,6 +243,11 @@ const char* mstf_status_string(int32_t s) {
   }
 }
 
+int mstf_attention_kernel_count(const mstf_cache* h) {
+  if (!h) return MSTF_EINVAL;
+  return uses_reg_kernel(h->view.kpad[0], h->view.kpad[1]) ? 1 : 2;
+}
+
 // Dev tooling, not declared in include/mustafar.h: per-CTA {start ns, end ns, smid} of the last
 // attention launch made with MSTF_TRACE set.
 int mstf_dev_trace(void* host, int32_t n) { return copy_trace(host, n) == cudaSuccess ? MSTF_OK : MSTF_ECUDA; }

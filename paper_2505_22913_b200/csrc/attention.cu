@@ -1473,6 +1473,13 @@ static int32_t pair_region_bytes(int32_t kp, bool v) {
   return (b + 127) / 128 * 128;
 }
 
+// Register-staged kernel (fused combine, stream-K) for equal K/V k_pad of 16, 32 or 40;
+// the TMA-staged kernel + separate combine otherwise.
+bool uses_reg_kernel(int32_t kpad_k, int32_t kpad_v) {
+  const int32_t nk = kpad_k / 8;
+  return kpad_k == kpad_v && (nk == 2 || nk == 4 || nk == 5);
+}
+
 AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_t uniform_items,
                         int32_t kpad_k, int32_t kpad_v, int32_t sm_count) {
   AttnPlan pl;
@@ -1502,8 +1509,7 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
   // (U+1)-int prefix array in shared memory; very large U keeps the split grid.
   pl.sk = 0;
   pl.sk_q = pl.sk_nb = pl.sk_grid = 0;
-  const int32_t nk = kpad_k / 8;
-  const bool reg_kernel = kpad_k == kpad_v && (nk == 2 || nk == 4 || nk == 5);
+  const bool reg_kernel = uses_reg_kernel(kpad_k, kpad_v);
   if (reg_kernel && total_items > 0 && total_items < (1ll << 30) && (uniform_items > 0 || U <= kMaxSkPrefix)) {
     int64_t grid = 2 * (int64_t)sm_count;
     if (grid > kMaxSkGrid) grid = kMaxSkGrid;
@@ -1561,7 +1567,7 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
       default: break;
     }
   }
-  const bool use_reg = (nk == nv) && (nk == 2 || nk == 4 || nk == 5);
+  const bool use_reg = uses_reg_kernel(c.kpad[0], c.kpad[1]);
   if (use_reg) {
     void (*rk)(AttnParams) = nullptr;
     switch (nk) {

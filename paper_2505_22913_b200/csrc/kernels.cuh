@@ -48,6 +48,7 @@ struct AttnPlan {
 // when it is the same for every unit, else 0.
 AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_t uniform_items,
                         int32_t kpad_k, int32_t kpad_v, int32_t sm_count);
+bool uses_reg_kernel(int32_t kpad_k, int32_t kpad_v);
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits);
 int32_t max_splits_for(int32_t U, int32_t capacity);
 

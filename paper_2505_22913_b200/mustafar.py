@@ -27,7 +27,8 @@ OUT_F32, OUT_F16 = 0, 1
 EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "mstf_cache_create",
            "mstf_cache_destroy", "mstf_cache_counts", "mstf_prune_compress_kv", "mstf_append_token",
            "mstf_workspace_bytes", "mstf_sparse_decode_attention", "mstf_dense_workspace_bytes",
-           "mstf_dense_decode_attention", "mstf_shard_units", "mstf_status_string", "mstf_build_info")
+           "mstf_dense_decode_attention", "mstf_shard_units", "mstf_attention_kernel_count",
+           "mstf_status_string", "mstf_build_info")
 
 
 class MustafarError(RuntimeError):
@@ -68,6 +69,7 @@ def lib() -> ctypes.CDLL:
         "mstf_dense_decode_attention": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, i32, vp, ctypes.c_float,
                                                        vp, i32, vp, sz, vp]),
         "mstf_shard_units": (ctypes.c_int, [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "mstf_attention_kernel_count": (ctypes.c_int, [vp]),
         "mstf_status_string": (ctypes.c_char_p, [i32]),
         "mstf_build_info": (ctypes.c_char_p, []),
     }
@@ -191,6 +193,13 @@ class MustafarCache:
             "n_comp": r["n_comp"].view(torch.int32),
             "n_win": r["n_win"].view(torch.int32),
         }
+
+    def attention_kernel_count(self) -> int:
+        """Kernels launched by one sparse_decode_attention call on this cache."""
+        n = lib().mstf_attention_kernel_count(self._h)
+        if n < 0:
+            _check("mstf_attention_kernel_count", n)
+        return n
 
     def counts(self):
         U = self.units

@@ -108,6 +108,19 @@ def test_host_validation_before_launch(L):
         L.mstf_cache_destroy(h)
 
 
+@pytest.mark.parametrize("kk,kv,n", [(39, 39, 1), (32, 32, 1), (16, 16, 1), (64, 64, 2), (39, 64, 2), (128, 128, 2)])
+def test_attention_kernel_count(L, kk, kv, n):
+    """s=.7 (k_pad 40) and friends use the register-staged kernel with the fused combine (one
+    launch); other k_pad use the TMA-staged kernel plus a combine kernel (two launches)."""
+    st, h = _fake_cache(L, keep_k=kk, keep_v=kv)
+    assert st == 0
+    try:
+        assert L.mstf_attention_kernel_count(h) == n
+    finally:
+        L.mstf_cache_destroy(h)
+    assert L.mstf_attention_kernel_count(None) == -1
+
+
 def test_shard_units(L):
     got = [M.shard_units(512, 8, r) for r in range(8)]
     assert got == [(64 * r, 64 * (r + 1)) for r in range(8)]
