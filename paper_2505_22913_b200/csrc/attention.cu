@@ -1037,6 +1037,8 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
     }
     fence_mbar_init();
   }
+  pdl_launch_dependents();
+  pdl_wait();  // cache, counters and q may be written by the previous kernel in the stream
   if (p.sk && p.sk_nb == 0) {
     // ragged stream-K: warp 0 scans the per-unit item counts into smem
     int* pref = reinterpret_cast<int*>(smem + p.off_pref);
@@ -1589,8 +1591,7 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
     }
     cudaError_t e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
     if (e != cudaSuccess) return e;
-    rk<<<grid, 256, rsmem, s>>>(pr);
-    return cudaGetLastError();
+    return launch_pdl(rk, grid, dim3(256), (size_t)rsmem, s, pr);
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

@@ -136,6 +136,8 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
 __global__ void __launch_bounds__(64) append_kernel(CacheView c, const uint16_t* __restrict__ k_new,
                                                     const uint16_t* __restrict__ v_new) {
   const int u = blockIdx.x, x = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();
+  pdl_wait();  // the token and the counters may come from the previous kernel in the stream
   const int nc = c.n_comp[u], nw = c.n_win[u];
   const uint16_t* src = (x ? v_new : k_new) + (size_t)u * kD;
   const size_t rec = (size_t)u * c.cap + nc;
@@ -184,8 +186,7 @@ cudaError_t launch_prefill(const CacheView& c, const uint16_t* k, const uint16_t
 }
 
 cudaError_t launch_append(const CacheView& c, const uint16_t* k_new, const uint16_t* v_new, cudaStream_t s) {
-  append_kernel<<<c.U, 64, 0, s>>>(c, k_new, v_new);
-  return cudaGetLastError();
+  return launch_pdl(append_kernel, dim3(c.U), dim3(64), 0, s, c, k_new, v_new);
 }
 
 }  // namespace mstf

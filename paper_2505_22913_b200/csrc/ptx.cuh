@@ -76,4 +76,12 @@ __device__ __forceinline__ uint32_t lanemask_gt() {
   return m;
 }
 
+// Programmatic dependent launch (sm_90+). Kernels of the decode step are launched with
+// programmatic stream serialization (launch_pdl): they may be scheduled while the previous
+// kernel in the stream drains, run their prologue, and must call pdl_wait() before the
+// first global memory access that could depend on it. pdl_launch_dependents() lets the
+// next kernel be scheduled early. Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace mstf
