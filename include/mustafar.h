@@ -170,9 +170,9 @@ int mstf_dense_decode_attention(const void* k, const void* v, const int32_t* len
  * slices are contiguous in [B][Hq][d]. Host-only.                                      */
 int mstf_shard_units(int32_t units, int32_t world, int32_t rank, int32_t* u0, int32_t* u1);
 
-/* Number of kernels one mstf_sparse_decode_attention call on this cache launches (1 when
- * the split combine is fused into the attention kernel, 2 when a separate combine kernel
- * runs), or a negative status for a NULL handle. Host-only; lets callers count launches. */
+/* Number of kernels one mstf_sparse_decode_attention call on this cache launches (the
+ * attention kernel and the split combine), or a negative status for a NULL handle.
+ * Host-only; lets callers count launches. */
 int mstf_attention_kernel_count(const mstf_cache* cache);
 
 /* Human-readable status (static string). */

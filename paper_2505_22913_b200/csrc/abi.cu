@@ -245,7 +245,8 @@ const char* mstf_status_string(int32_t s) {
 
 int mstf_attention_kernel_count(const mstf_cache* h) {
   if (!h) return MSTF_EINVAL;
-  return uses_reg_kernel(h->view.kpad[0], h->view.kpad[1]) ? 1 : 2;
+  // register kernel (stream-K) + stream-K combine, or TMA kernel (split grid) + combine
+  return 2;
 }
 
 // Dev tooling, not declared in include/mustafar.h: per-CTA {start ns, end ns, smid} of the last

@@ -35,6 +35,7 @@
 //     and 32t+4s+{2,3} (a2/a3, b1).
 //   V mma, m-tile i: row r <-> channel 8r+i, i.e. lane (g,t) expands bitmap bytes g and
 //     g+8 of tokens 2t, 2t+1, 2t+8, 2t+9.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -58,12 +59,17 @@ struct AttnParams {
   uint32_t off_handoff;             // byte offset of the K->V mailbox (split kernel)
   uint32_t reg_k, reg_v;            // per-warp pair-array region bytes (K, V)
   int* tickets;                     // [U] arrival counters for the fused combine
-  int32_t sk;                       // 1: stream-K schedule (grid = CTAs), 0: split grid (S, U)
-  int32_t sk_q;                     // stream-K: items per CTA
+  int32_t sk;                       // 1: register kernel, stream-K schedule; 0: split grid (S, U)
   int32_t sk_nb;                    // stream-K: items per unit if uniform, 0 = ragged (smem prefix)
   uint32_t off_pref;                // stream-K ragged: byte offset of the prefix array in smem
   int32_t trace;                    // dev: record per-CTA start/end/SM into g_trace
-  int32_t sk_rot;                   // dev: rotate the CTA -> item-range assignment
+  int32_t sk_qs;                    // stream-K: static items per worker (ranges [P*qs, (P+1)*qs))
+  int32_t sk_c;                     // stream-K: items per dynamic tail chunk
+  int32_t sk_nchunks;               // stream-K: dynamic tail chunks (0 = static only)
+  int32_t sk_total;                 // stream-K: total items
+  int* sk_ctr;                      // stream-K: [0] next tail chunk, [1] workers done (zero between calls)
+  int32_t sk_np;                    // stream-K: workers (warp pairs) = 4 * grid
+  int* sk_pref;                     // stream-K ragged: per-unit item prefix in the workspace (U+1)
   void* out;
   int out_f16;
 };
@@ -657,6 +663,7 @@ constexpr int kKVWarps = 8;
 constexpr int kThreadsKV = (kKVWarps + 1) * 32;
 constexpr int kBarBytesKV = 256;   // full[8], empty[8], hfull[8], hempty[8]
 constexpr int kHandoffBytes = 4 * 2 * 32 * 16;
+constexpr int kBarBytesReg = 256;  // register kernel: hfull, hempty, dfull, dempty [4 pairs][2]
 
 template <int NK, int NV, bool INTERLEAVED>
 __global__ void __launch_bounds__(kThreadsKV, 2) mstf_attn_kv_kernel(const AttnParams p) {
@@ -892,50 +899,11 @@ __global__ void __launch_bounds__(kThreadsKV, 2) mstf_attn_kv_kernel(const AttnP
 
 // Fused split combine: unit u's partials are [part_begin, part_begin + nparts) and `expected`
 // CTAs arrive; the last one to take a ticket merges them. Called by every thread of the CTA.
-__device__ __forceinline__ void combine_parts_if_last(const AttnParams& p, int u, int part_begin, int nparts, int expected) {
-  __shared__ int s_last;
-  __threadfence();  // publish this CTA's partials before its ticket
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int prev = atomicAdd(p.tickets + u, 1);
-    s_last = (prev == expected - 1);
-    if (s_last) p.tickets[u] = 0;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int G = p.G;
-  const int nthreads = blockDim.x;
-  // one warp per head; lane owns channels 4*lane..4*lane+3
-  for (int h = threadIdx.x >> 5; h < G; h += nthreads >> 5) {
-    const int lane = threadIdx.x & 31;
-    float M = -INFINITY;
-    for (int i = lane; i < nparts; i += 32) M = fmaxf(M, __ldcg(p.ws_ml + (((size_t)part_begin + i) * G + h) * 2));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float L = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-    for (int i = 0; i < nparts; ++i) {
-      const size_t pi = (size_t)part_begin + i;
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + (pi * G + h) * 2));
-      const float4 o = __ldcg(reinterpret_cast<const float4*>(p.ws_o + (pi * G + h) * kD + 4 * lane));
-      const float wgt = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
-      L += wgt * ml.y;
-      acc.x += wgt * o.x; acc.y += wgt * o.y; acc.z += wgt * o.z; acc.w += wgt * o.w;
-    }
-    const float inv = 1.f / L;
-    const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
-    if (p.out_f16) {
-      __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.out) + oi);
-      po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
-      po[1] = __floats2half2_rn(acc.z * inv, acc.w * inv);
-    } else {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oi) =
-          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    }
-  }
-}
+// Partial slots of unit u: [b1, b1 + n1) and [b2, b2 + n2); each slot holds kConsumerWarps
+// per-warp partials; n1 + n2 CTAs arrive.
+struct PartRanges {
+  int b1, n1, b2, n2;
+};
 
 // ---------------------------------------------------------------- K2 v4: register-staged (no TMA ring)
 // 4 K-warps + 4 V-warps per CTA; K-warp w and V-warp w+4 own the 16-token blocks
@@ -988,16 +956,30 @@ __device__ __forceinline__ void store_pairs(uint8_t* smem, const RawRegs<NCH>& r
   }
 }
 
-// Work schedule. A unit's work items are its compressed 16-token blocks (ceil(n_comp/16))
-// followed by its window row blocks (ceil(W/16)). Split mode (sk == 0): grid (S, U), CTA
-// (x, u) takes the x-th of S equal item ranges of unit u; partial slot u*S + x. Stream-K mode
-// (sk == 1): grid (C), the units' item lists are concatenated and CTA c takes items
-// [c*Q, (c+1)*Q), which may cross unit boundaries; the segment (c, u) uses partial slot c + u
-// (injective: along the monotone path of (c, u) segments c + u strictly increases), and unit
-// u's partials are the slots of CTAs first(u)..last(u).
-// Dev-only CTA timeline (MSTF_TRACE=1): {start ns, end ns, smid} per CTA.
-constexpr int kTraceMax = 8192;
-__device__ unsigned long long g_trace[3 * kTraceMax];
+// Work schedule (stream-K over warp pairs). A unit's work items are its compressed 16-token
+// blocks (ceil(n_comp/16)) followed by its window row blocks (ceil(W/16)); the units' item
+// lists are concatenated (N items). A worker is one K/V warp pair (K-warp w, V-warp w+4) and
+// NP = 4 * gridDim.x workers run independently (no CTA-wide sync after the prologue):
+//   static part: worker P takes items [P*qs, (P+1)*qs), which may cross unit boundaries;
+//     its segment (P, u) writes partial slot P + u.
+//   dynamic tail: items [NP*qs, N) in chunks of sk_c items; a worker that runs out of work
+//     grabs the next chunk from an atomic counter (equal-work workers run at data-dependent
+//     speeds, measured with tools/trace_ctas.py, so a purely static split ends with its
+//     slowest worker); segment (k, u) of chunk k writes slot NP + U + k + u.
+// Both slot maps are injective (along a monotone path of (P|k, u) pairs the sum strictly
+// increases) and their ranges are disjoint. Unit u's partial slots are those of the workers /
+// chunks overlapping it, a pure function of u (unit_parts); mstf_sk_combine_kernel merges them
+// (a9) in the next launch (programmatic dependent launch hides its start-up).
+// Segments never drain the K -> V pipeline: the K-warp publishes each segment's descriptor
+// {unit, lo, hi, slot} into a 2-deep mbarrier-guarded ring and streams on into the next
+// segment; the V-warp consumes descriptors in order. Each warp writes its half of the
+// partial (K: m, l per head; V: o per head) when it leaves a segment.
+
+// Dev-only CTA timeline (MSTF_TRACE=1): per CTA {start ns, end ns, smid, nseg, (seg end,
+// after ticket/combine) x 10} recorded by warp pair 0.
+constexpr int kTraceMax = 4096;
+constexpr int kTraceW = 24;
+__device__ unsigned long long g_trace[kTraceW * kTraceMax];
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1009,161 +991,164 @@ __device__ __forceinline__ unsigned smid() {
   return r;
 }
 
-// Stream-K: first item of unit u (u = U gives the total). Ragged caches read the prefix array
-// the CTA built in shared memory; recomputed from the params where needed (no live registers).
+// First item of unit u (u = U gives N). Ragged caches read the prefix array the CTA built
+// in shared memory; recomputed from the params where needed (no live registers).
 __device__ __forceinline__ int unit_start(const AttnParams& p, const uint8_t* smem, int u) {
   return p.sk_nb ? u * p.sk_nb : reinterpret_cast<const int*>(smem + p.off_pref)[u];
+}
+
+// Unit containing item `it`.
+__device__ __forceinline__ int unit_of_item(const AttnParams& p, const uint8_t* smem, int it) {
+  if (p.sk_nb) return it / p.sk_nb;
+  int lo = 0, hi = p.c.U;  // largest u with start(u) <= it
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (unit_start(p, smem, mid) <= it) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Partial slots of unit u (first item us, end item ue): static workers, then tail chunks,
+// overlapping it.
+__device__ __forceinline__ PartRanges unit_parts(const AttnParams& p, int u, int us, int ue) {
+  const int NP = p.sk_np;
+  const int s_end = min(NP * p.sk_qs, p.sk_total);
+  PartRanges r{0, 0, 0, 0};
+  if (us < s_end) {
+    const int cf = us / p.sk_qs, cl = (min(ue, s_end) - 1) / p.sk_qs;
+    r.b1 = cf + u;
+    r.n1 = cl - cf + 1;
+  }
+  if (ue > s_end) {
+    const int kf = (max(us, s_end) - s_end) / p.sk_c, kl = (ue - 1 - s_end) / p.sk_c;
+    r.b2 = NP + p.c.U + kf + u;
+    r.n2 = kl - kf + 1;
+  }
+  return r;
 }
 
 template <int NK, int NV>
 __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(smem);  // [pair][2] K -> V block handoff
   uint64_t* hempty = hfull + 8;
-  uint4* handoff = reinterpret_cast<uint4*>(smem + 128);
+  uint64_t* dfull = hfull + 16;                         // [pair][2] segment descriptors
+  uint64_t* dempty = hfull + 24;
+  uint4* handoff = reinterpret_cast<uint4*>(smem + kBarBytesReg);
+  __shared__ int4 s_desc[4][2];                         // {unit, lo, hi, slot}; unit < 0: end
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CacheView& c = p.c;
   const int nwb = c.W > 0 ? (c.W + 15) / 16 : 0;  // window row blocks per unit
-  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
-  if (p.trace && threadIdx.x == 0 && cta < kTraceMax) {
-    g_trace[3 * cta] = global_ns();
-    g_trace[3 * cta + 2] = smid();
+  const int cta = blockIdx.x;
+  const bool tracing = p.trace && cta < kTraceMax;
+  if (tracing && threadIdx.x == 0) {
+    g_trace[kTraceW * cta] = global_ns();
+    g_trace[kTraceW * cta + 2] = smid();
+    g_trace[kTraceW * cta + 3] = 0;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 8; ++i) {
-      mbar_init(&hfull[i], 1);
-      mbar_init(&hempty[i], 1);
-    }
+    for (int i = 0; i < 32; ++i) mbar_init(&hfull[i], 1);
     fence_mbar_init();
   }
   pdl_launch_dependents();
   pdl_wait();  // cache, counters and q may be written by the previous kernel in the stream
-  if (p.sk && p.sk_nb == 0) {
-    // ragged stream-K: warp 0 scans the per-unit item counts into smem
+  if (p.sk_nb == 0 && warp == 0) {
+    // ragged cache: warp 0 scans the per-unit item counts into smem (CTA 0 also publishes
+    // them for the combine kernel)
     int* pref = reinterpret_cast<int*>(smem + p.off_pref);
-    if (warp == 0) {
-      int carry = 0;
-      for (int u0 = 0; u0 < c.U; u0 += 32) {
-        const int uu = u0 + lane;
-        const int items = uu < c.U ? (c.n_comp[uu] + 15) / 16 + nwb : 0;
-        int incl = items;
+    int carry = 0;
+    for (int u0 = 0; u0 < c.U; u0 += 32) {
+      const int uu = u0 + lane;
+      const int items = uu < c.U ? (c.n_comp[uu] + 15) / 16 + nwb : 0;
+      int incl = items;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        if (uu < c.U) pref[uu] = carry + incl - items;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      if (lane == 0) pref[c.U] = carry;
+      if (uu < c.U) {
+        pref[uu] = carry + incl - items;
+        if (cta == 0) p.sk_pref[uu] = carry + incl - items;
+      }
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      pref[c.U] = carry;
+      if (cta == 0) p.sk_pref[c.U] = carry;
     }
   }
-  __syncthreads();
-
-  // Segment bookkeeping lives in shared memory (re-read where used) so that it does not hold
-  // registers across the block loops: [0] unit, [1] first item, [2] CTA end item,
-  // [3] lo, [4] hi (unit-relative), [5] unit start, [6] unit end (absolute items).
-  __shared__ int s_seg[8];
-  const volatile int* seg = s_seg;
-  if (threadIdx.x == 0) {
-    int u0, it0, it_end0;
-    if (p.sk) {
-      it0 = ((blockIdx.x + p.sk_rot) % gridDim.x) * p.sk_q;
-      it_end0 = min(it0 + p.sk_q, unit_start(p, smem, c.U));
-      if (p.sk_nb == 0) {
-        int lo = 0, hi = c.U;  // largest u with start(u) <= it0
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (unit_start(p, smem, mid) <= it0) lo = mid; else hi = mid;
-        }
-        u0 = lo;
-      } else {
-        u0 = it0 / p.sk_nb;
-      }
-    } else {
-      u0 = blockIdx.y;
-      const int items = (c.n_comp[u0] + 15) / 16 + nwb;
-      const int per = (items + gridDim.x - 1) / gridDim.x;
-      it0 = min((int)blockIdx.x * per, items);
-      it_end0 = min(it0 + per, items);
-    }
-    s_seg[0] = u0; s_seg[1] = it0; s_seg[2] = it_end0;
-  }
+  __syncthreads();  // barriers and prefix visible; the only CTA-wide barrier
 
   const bool is_k = warp < 4;
   const int w = warp & 3;
   const int g = lane >> 2, t = lane & 3;
   const uint32_t ybase = p.off_pairs + (is_k ? (uint32_t)w * p.reg_k : 4 * p.reg_k + (uint32_t)w * p.reg_v);
-  int blk = 0;  // handoff sequence number (K-warp w and V-warp w+4 walk the same blocks)
-
-  // Segment prologue/epilogue shared by both roles; each role runs its own segment loop so
-  // that registers are allocated per role.
-  auto segment_begin = [&]() {
-    // ---- segment: unit u, unit-relative items [lo, hi)
-    if (threadIdx.x == 0) {
-      const int u0 = s_seg[0], it0 = s_seg[1], it_end0 = s_seg[2];
-      const int ustart = p.sk ? unit_start(p, smem, u0) : 0;
-      const int uend = p.sk ? unit_start(p, smem, u0 + 1) : it_end0;
-      s_seg[3] = it0 - ustart;
-      s_seg[4] = min(it_end0, uend) - ustart;
-      s_seg[5] = ustart;
-      s_seg[6] = uend;
-    }
-    __syncthreads();
-  };
-  auto segment_end = [&]() -> bool {
-    {
-      const int uu = seg[0];
-      if (p.sk) {
-        const int cf = seg[5] / p.sk_q, cl = (seg[6] - 1) / p.sk_q;
-        combine_parts_if_last(p, uu, (cf + uu) * kConsumerWarps, (cl - cf + 1) * kConsumerWarps, cl - cf + 1);
-      } else {
-        combine_parts_if_last(p, uu, uu * gridDim.x * kConsumerWarps, gridDim.x * kConsumerWarps, gridDim.x);
-      }
-    }
-    if (!p.sk || seg[2] <= seg[6]) return false;
-    __syncthreads();  // everyone has read this segment's bookkeeping
-    if (threadIdx.x == 0) {
-      s_seg[1] = s_seg[6];
-      s_seg[0] = s_seg[0] + 1;
-    }
-    return true;
-  };
+  const int NP = p.sk_np;
+  int blk = 0;   // block handoff sequence number (K-warp w and V-warp w+4 walk the same blocks)
+  int nseg = 0;  // segment descriptor sequence number
 
   if (is_k) {
+    // ================= K-warp: schedule, scores + online softmax, P^T -> V-warp
+    // Bookkeeping in shared memory, written by lane 0 (keeps it out of registers): [0] unit,
+    // [1] next item, [2] range end, [3] lo, [4] hi (unit-relative), [5] slot base,
+    // [6] prefetched tail chunk, [7] more work, [8] unit end (absolute).
+    __shared__ int s_seg[4][10];
+    volatile int* sg = s_seg[w];
+    auto set_bounds = [&]() {  // lane 0
+      const int u0 = sg[0];
+      const int us = unit_start(p, smem, u0), ue = unit_start(p, smem, u0 + 1);
+      sg[3] = sg[1] - us;
+      sg[4] = min((int)sg[2], ue) - us;
+      sg[8] = ue;
+    };
+    auto publish = [&](int4 d) {  // lane 0: descriptor for the V-warp
+      const int ds = nseg & 1;
+      if (nseg >= 2) mbar_wait(&dempty[2 * w + ds], ((nseg >> 1) - 1) & 1);
+      s_desc[w][ds] = d;
+      mbar_arrive(&dfull[2 * w + ds]);
+    };
+    if (lane == 0) {
+      const int P = (int)blockIdx.x * 4 + w;
+      const int it0 = P * p.sk_qs;
+      sg[7] = it0 < p.sk_total;
+      if (sg[7]) {
+        sg[1] = it0;
+        sg[2] = min(it0 + p.sk_qs, p.sk_total);
+        sg[0] = unit_of_item(p, smem, it0);
+        sg[5] = P;
+        set_bounds();
+      }
+      // first tail grab now: its latency hides behind the static range
+      sg[6] = p.sk_nchunks > 0 ? atomicAdd(p.sk_ctr, 1) : 0;
+    }
+    __syncwarp();
+    KState st;
+    int qu = -1;  // unit whose q is in st.qf
     for (;;) {
-      segment_begin();
-      const int u = seg[0];
+      if (lane == 0) publish(sg[7] ? make_int4(sg[0], sg[3], sg[4], sg[5] + sg[0]) : make_int4(-1, 0, 0, 0));
+      ++nseg;
+      __syncwarp();
+      if (!sg[7]) break;
+      const int u = sg[0];
       const int n = c.n_comp[u];
       const int nbc = (n + 15) / 16;
-      const int bbeg = min((int)seg[3], nbc), bend = min((int)seg[4], nbc);
-      // window items x in [max(lo, nbc), hi) go to warp (x - lo) % 4 (computed after the main loop)
-      auto first_window_item = [&]() {
-        const int lo = seg[3];
-        const int xw0 = max(lo, nbc);
-        return xw0 + ((w - (xw0 - lo)) % 4 + 4) % 4;
-      };
-      auto part_index = [&]() -> size_t {
-        const int uu = seg[0];
-        const int slot = p.sk ? (int)((blockIdx.x + p.sk_rot) % gridDim.x) + uu : uu * (int)gridDim.x + (int)blockIdx.x;
-        return (size_t)slot * kConsumerWarps + w;
-      };
-
-      // ================= K-warp
-      KState st;
+      const int bbeg = min((int)sg[3], nbc), bend = min((int)sg[4], nbc);
       st.m0 = st.m1 = -INFINITY;
       st.l0 = st.l1 = 0.f;
-      if (g < p.G) {
-        const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + g) * kD + 32 * t);
+      if (u != qu) {
+        qu = u;
+        if (g < p.G) {
+          const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + g) * kD + 32 * t);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint4 x = qp[i];
-          st.qf[4 * i] = x.x; st.qf[4 * i + 1] = x.y; st.qf[4 * i + 2] = x.z; st.qf[4 * i + 3] = x.w;
+          for (int i = 0; i < 4; ++i) {
+            const uint4 x = qp[i];
+            st.qf[4 * i] = x.x; st.qf[4 * i + 1] = x.y; st.qf[4 * i + 2] = x.z; st.qf[4 * i + 3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) st.qf[i] = 0;
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) st.qf[i] = 0;
       }
       auto handoff_put = [&](const uint4 hh) {
         const int hs = blk & 1;
@@ -1192,26 +1177,25 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         handoff_put(k_block(kr, g < nvalid, g + 8 < nvalid, st, p.scale_log2));
       };
       {
-        // unit base pointers are re-derived per load (seg[0], params) to save registers
+        // unit base pointers are re-derived per load (sg[0], params) to save registers
         auto load = [&](RawRegs<NK>& rr, int bb) {
-          const size_t ub = (size_t)seg[0] * c.cap;
+          const size_t ub = (size_t)sg[0] * c.cap;
           load_raw<NK>(rr, c.val[0] + ub * c.kpad[0], c.bm[0] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
         };
         RawRegs<NK> ra, rb;
-        int b = bbeg + w;
+        int b = bbeg;
         if (b < bend) load(ra, b);
         while (b < bend) {
-          if (b + 4 < bend) load(rb, b + 4);
+          if (b + 1 < bend) load(rb, b + 1);
           k_step(ra, b);
-          b += 4;
-          if (b >= bend) break;
-          if (b + 4 < bend) load(ra, b + 4);
+          if (++b >= bend) break;
+          if (b + 1 < bend) load(ra, b + 1);
           k_step(rb, b);
-          b += 4;
+          ++b;
         }
       }
       const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
-      for (int x = first_window_item(), hi = seg[4]; x < hi; x += 4) {
+      for (int x = max((int)sg[3], nbc), hi = sg[4]; x < hi; ++x) {
         DenseBlock db;
         db.k = c.win[0] + (size_t)u * c.W * kD;
         db.v = c.win[1] + (size_t)u * c.W * kD;
@@ -1244,34 +1228,61 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         l0 += __shfl_xor_sync(0xffffffffu, l0, o);
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
       }
-      float* ml = p.ws_ml + part_index() * p.G * 2;
+      float* ml = p.ws_ml + (size_t)(sg[5] + u) * p.G * 2;
       if (g == 0) {
         if (2 * t < p.G) { ml[4 * t] = st.m0; ml[4 * t + 1] = l0; }
         if (2 * t + 1 < p.G) { ml[4 * t + 2] = st.m1; ml[4 * t + 3] = l1; }
       }
-      if (!segment_end()) break;
+      __syncwarp();
+      if (lane == 0) {
+        if (tracing && w == 0) {
+          const int ns = (int)g_trace[kTraceW * cta + 3];
+          if (ns < 10) {
+            g_trace[kTraceW * cta + 4 + 2 * ns] = global_ns();
+            g_trace[kTraceW * cta + 5 + 2 * ns] = u;
+            g_trace[kTraceW * cta + 3] = ns + 1;
+          }
+        }
+        // advance: rest of the range in the next unit, else the next tail chunk, else done
+        if (sg[2] > sg[8]) {
+          sg[1] = sg[8];
+          sg[0] = sg[0] + 1;
+          set_bounds();
+        } else if (p.sk_nchunks > 0 && sg[6] < p.sk_nchunks) {
+          const int k = sg[6];
+          const int it0 = min(NP * p.sk_qs, p.sk_total) + k * p.sk_c;
+          sg[1] = it0;
+          sg[2] = min(it0 + p.sk_c, p.sk_total);
+          sg[0] = unit_of_item(p, smem, it0);
+          sg[5] = NP + c.U + k;
+          set_bounds();
+          sg[6] = atomicAdd(p.sk_ctr, 1);  // prefetch the following chunk
+        } else {
+          sg[7] = 0;
+          if (p.sk_nchunks > 0 && atomicAdd(p.sk_ctr + 1, 1) == NP - 1) {
+            // last worker to run out: every grab has happened; reset for the next call
+            p.sk_ctr[0] = 0;
+            p.sk_ctr[1] = 0;
+          }
+        }
+      }
+      __syncwarp();
     }
-    if (p.trace && threadIdx.x == 0 && cta < kTraceMax) g_trace[3 * cta + 1] = global_ns();
+    if (tracing && w == 0 && lane == 0) g_trace[kTraceW * cta + 1] = global_ns();
   } else {
+    // ================= V-warp: P.V over the segments the K-warp publishes
     for (;;) {
-      segment_begin();
-      const int u = seg[0];
+      const int ds = nseg & 1;
+      mbar_wait(&dfull[2 * w + ds], (nseg >> 1) & 1);
+      const int4 d = s_desc[w][ds];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dempty[2 * w + ds]);
+      ++nseg;
+      const int u = d.x;
+      if (u < 0) break;
       const int n = c.n_comp[u];
       const int nbc = (n + 15) / 16;
-      const int bbeg = min((int)seg[3], nbc), bend = min((int)seg[4], nbc);
-      // window items x in [max(lo, nbc), hi) go to warp (x - lo) % 4 (computed after the main loop)
-      auto first_window_item = [&]() {
-        const int lo = seg[3];
-        const int xw0 = max(lo, nbc);
-        return xw0 + ((w - (xw0 - lo)) % 4 + 4) % 4;
-      };
-      auto part_index = [&]() -> size_t {
-        const int uu = seg[0];
-        const int slot = p.sk ? (int)((blockIdx.x + p.sk_rot) % gridDim.x) + uu : uu * (int)gridDim.x + (int)blockIdx.x;
-        return (size_t)slot * kConsumerWarps + w;
-      };
-
-      // ================= V-warp
+      const int bbeg = min(d.y, nbc), bend = min(d.z, nbc);
       float acc[2][4][4];
 #pragma unroll
       for (int e = 0; e < 2; ++e)
@@ -1314,26 +1325,22 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         v_block(vr, handoff_get(), acc);
       };
       {
-        // unit base pointers are re-derived per load (seg[0], params) to save registers
-        auto load = [&](RawRegs<NV>& rr, int bb) {
-          const size_t ub = (size_t)seg[0] * c.cap;
-          load_raw<NV>(rr, c.val[1] + ub * c.kpad[1], c.bm[1] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
-        };
+        const uint16_t* vals = c.val[1] + (size_t)u * c.cap * c.kpad[1];
+        const uint64_t* bms = c.bm[1] + (size_t)u * c.cap * kTiles;
         RawRegs<NV> ra, rb;
-        int b = bbeg + w;
-        if (b < bend) load(ra, b);
+        int b = bbeg;
+        if (b < bend) load_raw<NV>(ra, vals, bms, b * 16, min(16, n - b * 16), lane);
         while (b < bend) {
-          if (b + 4 < bend) load(rb, b + 4);
+          if (b + 1 < bend) load_raw<NV>(rb, vals, bms, (b + 1) * 16, min(16, n - (b + 1) * 16), lane);
           v_step(ra);
-          b += 4;
-          if (b >= bend) break;
-          if (b + 4 < bend) load(ra, b + 4);
+          if (++b >= bend) break;
+          if (b + 1 < bend) load_raw<NV>(ra, vals, bms, (b + 1) * 16, min(16, n - (b + 1) * 16), lane);
           v_step(rb);
-          b += 4;
+          ++b;
         }
       }
       const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
-      for (int x = first_window_item(), hi = seg[4]; x < hi; x += 4) {
+      for (int x = max(d.y, nbc); x < d.z; ++x) {
         DenseBlock db;
         db.k = c.win[0] + (size_t)u * c.W * kD;
         db.v = c.win[1] + (size_t)u * c.W * kD;
@@ -1358,7 +1365,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         }
         v_block(vr, handoff_get(), acc);
       }
-      float* o = p.ws_o + part_index() * p.G * kD;
+      float* o = p.ws_o + (size_t)d.w * p.G * kD;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int h = 2 * t + hh;
@@ -1371,8 +1378,65 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
           }
         }
       }
-      if (!segment_end()) break;
     }
+  }
+}
+
+// a9 for the stream-K schedule: one CTA (G warps) per unit merges the unit's partial slots
+// (unit_parts). Phase 1: lanes load (m, l) of different slots in parallel and reduce the max
+// with shuffles; phase 2: a branch-free loop accumulates w_i * o_i (weights broadcast from
+// the lane that holds them), so the slot loads of successive iterations overlap.
+__global__ void __launch_bounds__(kMaxGroup * 32) mstf_sk_combine_kernel(const AttnParams p) {
+  pdl_launch_dependents();
+  pdl_wait();  // partials come from the attention kernel just before
+  const int u = blockIdx.x, h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = p.G;
+  if (h >= G) return;
+  const int us = p.sk_nb ? u * p.sk_nb : p.sk_pref[u];
+  const int ue = p.sk_nb ? (u + 1) * p.sk_nb : p.sk_pref[u + 1];
+  const PartRanges r = unit_parts(p, u, us, ue);
+  const int np = r.n1 + r.n2;
+  auto slot = [&](int i) -> size_t { return i < r.n1 ? (size_t)(r.b1 + i) : (size_t)(r.b2 + i - r.n1); };
+  float m_max = -INFINITY, l_sum = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int kB = 16;  // slots per batch: all their loads are issued before any math
+  for (int i0 = 0; i0 < np; i0 += kB) {
+    const int cnt = min(kB, np - i0);
+    float2 ml = make_float2(-INFINITY, 0.f);
+    if (lane < cnt) ml = *reinterpret_cast<const float2*>(p.ws_ml + (slot(i0 + lane) * G + h) * 2);
+    float4 v[kB];
+#pragma unroll
+    for (int i = 0; i < kB; ++i)
+      v[i] = i < cnt ? *(reinterpret_cast<const float4*>(p.ws_o + (slot(i0 + i) * G + h) * kD) + lane)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    float mb = ml.x;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    const float mn = fmaxf(m_max, mb);
+    if (mn == -INFINITY) continue;  // warp-uniform: no tokens in this batch nor before
+    const float a = exp2f(m_max - mn);
+    const float wgt = ml.x == -INFINITY ? 0.f : exp2f(ml.x - mn);
+    float lb = wgt * ml.y;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) lb += __shfl_xor_sync(0xffffffffu, lb, o);
+    l_sum = l_sum * a + lb;
+    acc.x *= a; acc.y *= a; acc.z *= a; acc.w *= a;
+    m_max = mn;
+#pragma unroll
+    for (int i = 0; i < kB; ++i) {
+      const float wi = __shfl_sync(0xffffffffu, wgt, i);
+      acc.x += wi * v[i].x; acc.y += wi * v[i].y; acc.z += wi * v[i].z; acc.w += wi * v[i].w;
+    }
+  }
+  const float inv = 1.f / l_sum;
+  const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
+  if (p.out_f16) {
+    __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.out) + oi);
+    po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
+    po[1] = __floats2half2_rn(acc.z * inv, acc.w * inv);
+  } else {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oi) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   }
 }
 
@@ -1445,13 +1509,20 @@ int32_t max_splits_for(int32_t U, int32_t capacity) {
   return s < 1 ? 1 : s;
 }
 
-static size_t ticket_bytes(int32_t U) { return ((size_t)U * sizeof(int) + 255) / 256 * 256; }
+// Workspace header: [U] unit tickets (kv kernel) + [2] stream-K tail counters (zero between
+// calls), then the stream-K per-unit prefix [U+1].
+static size_t ticket_bytes(int32_t U) {
+  return ((size_t)(U + 2) * sizeof(int) + 255) / 256 * 256 + ((size_t)(U + 1) * sizeof(int) + 255) / 256 * 256;
+}
 
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits) {
-  // split mode uses U*S partial slots, stream-K at most grid + U (grid <= kMaxSkGrid)
-  size_t slots = (size_t)U * max_splits;
-  if (slots < (size_t)U + kMaxSkGrid) slots = (size_t)U + kMaxSkGrid;
-  const size_t parts = slots * kConsumerWarps;
+  // split grid (TMA kernel): U*S*4 per-warp partials; stream-K (register kernel): one partial
+  // per slot, at most NP + U (static) + chunks + U (tail), NP = 4 * grid <= 4 * kMaxSkGrid and
+  // chunks <= kSkChunksPerWorker * NP
+  size_t parts = (size_t)U * max_splits * kConsumerWarps;
+  const size_t np = 4 * (size_t)kMaxSkGrid;
+  const size_t sk_parts = 2 * (size_t)U + np * (1 + kSkChunksPerWorker) + 1;
+  if (parts < sk_parts) parts = sk_parts;
   return ticket_bytes(U) + parts * G * (kD + 2) * sizeof(float) + 256;
 }
 
@@ -1506,22 +1577,40 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
     if (t < best_t - 1e-9) { best_t = t; best = s; }
   }
   pl.splits = best;
-  // Stream-K schedule for the register-staged kernel: one wave of 2 CTAs per SM with equal item
-  // counts (no idle SMs in a partial wave, one prologue/epilogue per CTA). Ragged units need a
-  // (U+1)-int prefix array in shared memory; very large U keeps the split grid.
+  // Stream-K schedule for the register-staged kernel (see the schedule comment above the
+  // kernel): one wave of 2 CTAs per SM = 8 warp-pair workers per SM; each worker gets a
+  // static (100 - tail)% share of the items, the rest is handed out as dynamic chunks
+  // (<= kSkChunksPerWorker per worker). Ragged units need a (U+1)-int prefix array in shared
+  // memory, so very large ragged U falls back to the TMA kernel's split grid.
   pl.sk = 0;
-  pl.sk_q = pl.sk_nb = pl.sk_grid = 0;
-  const bool reg_kernel = uses_reg_kernel(kpad_k, kpad_v);
-  if (reg_kernel && total_items > 0 && total_items < (1ll << 30) && (uniform_items > 0 || U <= kMaxSkPrefix)) {
+  pl.sk_qs = pl.sk_nb = pl.sk_grid = pl.sk_c = pl.sk_nchunks = 0;
+  pl.sk_total = 0;
+  if (uses_reg_kernel(kpad_k, kpad_v) && total_items > 0 && total_items < (1ll << 30) &&
+      (uniform_items > 0 || U <= kMaxSkPrefix)) {
     int64_t grid = 2 * (int64_t)sm_count;
     if (grid > kMaxSkGrid) grid = kMaxSkGrid;
-    const int64_t min_q = 8;  // >= 2 blocks per warp to amortise the prologue
+    const int64_t min_q = 8;  // >= 2 items per worker to amortise the segment prologue
     if (grid > (total_items + min_q - 1) / min_q) grid = (total_items + min_q - 1) / min_q;
     if (grid < 1) grid = 1;
-    const int64_t q = (total_items + grid - 1) / grid;
+    const int64_t np = 4 * grid;
+    int tail_pct = 0;  // measured: chunk segments cost more than the balance they buy
+    if (const char* e = std::getenv("MSTF_SKTAIL")) tail_pct = std::atoi(e);  // tuning override
+    int64_t min_chunk = 2;
+    if (const char* e = std::getenv("MSTF_SKC")) min_chunk = std::max<int64_t>(1, std::atoi(e));
+    const int64_t q = (total_items + np - 1) / np;
+    int64_t qs = q, chunk = 0, nchunks = 0;
+    if (tail_pct > 0 && q >= 8) {
+      qs = total_items * (100 - tail_pct) / (100 * np);
+      const int64_t tail = total_items - np * qs;
+      chunk = std::max(min_chunk, (tail + kSkChunksPerWorker * np - 1) / (kSkChunksPerWorker * np));
+      nchunks = (tail + chunk - 1) / chunk;
+    }
     pl.sk = 1;
-    pl.sk_q = (int32_t)q;
-    pl.sk_grid = (int32_t)((total_items + q - 1) / q);
+    pl.sk_qs = (int32_t)qs;
+    pl.sk_grid = (int32_t)grid;
+    pl.sk_c = (int32_t)chunk;
+    pl.sk_nchunks = (int32_t)nchunks;
+    pl.sk_total = (int32_t)total_items;
     pl.sk_nb = uniform_items;
   }
   return pl;
@@ -1543,19 +1632,22 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.off_handoff = p.off_pairs + plan.pair_bytes;
   p.reg_k = plan.reg_k;
   p.reg_v = plan.reg_v;
-  // partial slots: U*S (split grid) or grid + U (stream-K, see UnitSched)
-  const size_t parts = (plan.sk ? (size_t)c.U + plan.sk_grid : (size_t)c.U * plan.splits) * kConsumerWarps;
+  // partials: U*S*4 per-warp (TMA kernel, split grid) or one per slot, NP + 2U + chunks
+  // (register kernel, stream-K)
+  const size_t parts = plan.sk ? 4 * (size_t)plan.sk_grid + 2 * (size_t)c.U + plan.sk_nchunks
+                               : (size_t)c.U * plan.splits * kConsumerWarps;
   p.tickets = reinterpret_cast<int*>(ws);  // [U] ticket counters at a fixed place (zero between calls)
   p.ws_o = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ticket_bytes(c.U));
   p.ws_ml = p.ws_o + parts * G * kD;
   p.out = out;
   p.out_f16 = out_f16;
   p.sk = 0;
-  p.sk_q = p.sk_nb = 0;
+  p.sk_qs = p.sk_nb = p.sk_c = p.sk_nchunks = p.sk_total = 0;
+  p.sk_ctr = p.tickets + c.U;
+  p.sk_pref = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ((size_t)(c.U + 2) * sizeof(int) + 255) / 256 * 256);
+  p.sk_np = 0;
   p.off_pref = 0;
   p.trace = std::getenv("MSTF_TRACE") != nullptr;  // dev timeline (tools/trace_ctas.py)
-  p.sk_rot = 0;
-  if (const char* e = std::getenv("MSTF_SKROT")) p.sk_rot = std::atoi(e);
   const int smem = kBarBytesKV + plan.nstage * plan.stage_bytes + plan.pair_bytes + kHandoffBytes;
   // kernel choice: register-staged interleaved kernel for kpad <= 40 (nk <= 5); TMA-staged kernel
   // with contiguous pair arrays for kpad >= 48 (interleaving aliases banks at ~50% density).
@@ -1569,8 +1661,7 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
       default: break;
     }
   }
-  const bool use_reg = uses_reg_kernel(c.kpad[0], c.kpad[1]);
-  if (use_reg) {
+  if (plan.sk) {  // register-staged kernel, stream-K schedule
     void (*rk)(AttnParams) = nullptr;
     switch (nk) {
       case 2: rk = mstf_attn_reg_kernel<2, 2>; break;
@@ -1578,20 +1669,23 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
       default: rk = mstf_attn_reg_kernel<5, 5>; break;
     }
     AttnParams pr = p;
-    pr.off_pairs = 128 + kHandoffBytes;
+    pr.off_pairs = kBarBytesReg + kHandoffBytes;
     int rsmem = pr.off_pairs + plan.pair_bytes;
-    dim3 grid(plan.splits, c.U);
-    if (plan.sk) {
-      pr.sk = 1;
-      pr.sk_q = plan.sk_q;
-      pr.sk_nb = plan.sk_nb;
-      pr.off_pref = (uint32_t)rsmem;
-      if (plan.sk_nb == 0) rsmem += (c.U + 1) * (int)sizeof(int);
-      grid = dim3(plan.sk_grid, 1);
-    }
+    pr.sk = 1;
+    pr.sk_qs = plan.sk_qs;
+    pr.sk_c = plan.sk_c;
+    pr.sk_nchunks = plan.sk_nchunks;
+    pr.sk_total = plan.sk_total;
+    pr.sk_nb = plan.sk_nb;
+    pr.sk_np = 4 * plan.sk_grid;
+    pr.off_pref = (uint32_t)rsmem;
+    if (plan.sk_nb == 0) rsmem += (c.U + 1) * (int)sizeof(int);
+    const dim3 grid(plan.sk_grid, 1);
     cudaError_t e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, rsmem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(rk, grid, dim3(256), (size_t)rsmem, s, pr);
+    e = launch_pdl(rk, grid, dim3(256), (size_t)rsmem, s, pr);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(mstf_sk_combine_kernel, dim3(c.U), dim3(32 * G), 0, s, pr);
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -1617,7 +1711,7 @@ cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const i
 }
 
 cudaError_t copy_trace(void* host, int n) {
-  if (n > 3 * kTraceMax) n = 3 * kTraceMax;
+  if (n > kTraceW * kTraceMax) n = kTraceW * kTraceMax;
   return cudaMemcpyFromSymbol(host, g_trace, n * sizeof(unsigned long long));
 }
 

@@ -3,12 +3,18 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <utility>
 
 namespace mstf {
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while its
 // predecessor in the stream drains; it must pdl_wait() before touching dependent memory.
+inline bool pdl_enabled() {  // MSTF_NOPDL=1 (dev): ordinary launches, e.g. for profiler timelines
+  static const bool on = std::getenv("MSTF_NOPDL") == nullptr;
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {
@@ -21,7 +27,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -32,6 +38,7 @@ constexpr int kConsumerWarps = 4;
 constexpr int kMaxGroup = 8;     // query heads per unit (mma N = 8)
 constexpr int kMaxSkGrid = 2 * 148;  // stream-K grid cap (2 CTAs per SM on a B200)
 constexpr int kMaxSkPrefix = 16384;  // ragged stream-K: max units (prefix array in smem)
+constexpr int kSkChunksPerWorker = 2;  // stream-K dynamic tail: at most this many chunks per warp pair
 
 // Device view of one cache (one tensor = K or V shares the same layout).
 struct CacheView {
@@ -59,7 +66,10 @@ struct AttnPlan {
   int32_t pair_bytes;    // per-CTA shifted pair arrays (4 warps x 16 tokens x K,V)
   int32_t reg_k, reg_v;  // per-warp region bytes
   int32_t sk;            // 1: stream-K schedule (register-staged kernel)
-  int32_t sk_q;          // items (16-token blocks) per CTA
+  int32_t sk_qs;         // static items (16-token blocks) per worker (warp pair)
+  int32_t sk_c;          // items per dynamic tail chunk
+  int32_t sk_nchunks;    // dynamic tail chunks
+  int32_t sk_total;      // total items
   int32_t sk_nb;         // items per unit when all units are equal, else 0
   int32_t sk_grid;       // CTAs
 };

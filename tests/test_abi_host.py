@@ -108,10 +108,10 @@ def test_host_validation_before_launch(L):
         L.mstf_cache_destroy(h)
 
 
-@pytest.mark.parametrize("kk,kv,n", [(39, 39, 1), (32, 32, 1), (16, 16, 1), (64, 64, 2), (39, 64, 2), (128, 128, 2)])
+@pytest.mark.parametrize("kk,kv,n", [(39, 39, 2), (32, 32, 2), (16, 16, 2), (64, 64, 2), (39, 64, 2), (128, 128, 2)])
 def test_attention_kernel_count(L, kk, kv, n):
-    """s=.7 (k_pad 40) and friends use the register-staged kernel with the fused combine (one
-    launch); other k_pad use the TMA-staged kernel plus a combine kernel (two launches)."""
+    """Every attention call is two launches: the attention kernel (register-staged stream-K or
+    TMA-staged split grid, chosen by k_pad) and the split combine."""
     st, h = _fake_cache(L, keep_k=kk, keep_v=kv)
     assert st == 0
     try:

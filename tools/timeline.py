@@ -15,9 +15,11 @@ for l in range(L):
     caches.append(c)
 q = synth.fp16_torch((U, G, 128), 7); kn = synth.fp16_torch((U, 128), 8); vn = synth.fp16_torch((U, 128), 9)
 out = torch.empty(U, G, 128, device="cuda", dtype=torch.float16)
+APPEND = os.environ.get("APPEND", "1") == "1"
 def step():
     for c in caches:
-        c.append_token(kn, vn)
+        if APPEND:
+            c.append_token(kn, vn)
         c.sparse_decode_attention(q, out=out)
 step(); torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -37,6 +39,7 @@ import collections
 agg = collections.defaultdict(list)
 for n, d, g in rows[len(rows) // 3:]:
     agg[n].append((d, g))
+print(os.environ.get("TAG", ""))
 for n, v in agg.items():
     ds = sorted(x[0] for x in v); gs = sorted(x[1] for x in v)
     print(f"{n:60s} n={len(v):3d} dur med {ds[len(ds)//2]:.1f} us  gap-before med {gs[len(gs)//2]:.1f} us")
