@@ -167,12 +167,11 @@ int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale
   if (!ws || !aligned16(ws) || ws_bytes < mstf_workspace_bytes(h)) return MSTF_EWORKSPACE;
   int32_t max_comp = 0;
   int64_t total_items = 0;
-  const int32_t nwb = h->view.W > 0 ? (h->view.W + 15) / 16 : 0;
-  int32_t uniform_items = (h->nc[0] + 15) / 16 + nwb;
+  int32_t uniform_items = sk_unit_cost(h->nc[0], h->view.W);
   for (int32_t u = 0; u < h->view.U; ++u) {
     if (h->nc[u] + h->nw[u] == 0) return MSTF_EEMPTY;
     if (h->nc[u] > max_comp) max_comp = h->nc[u];
-    const int32_t items = (h->nc[u] + 15) / 16 + nwb;
+    const int32_t items = sk_unit_cost(h->nc[u], h->view.W);
     total_items += items;
     if (items != uniform_items) uniform_items = 0;
   }

@@ -63,12 +63,13 @@ struct AttnParams {
   int32_t sk_nb;                    // stream-K: items per unit if uniform, 0 = ragged (smem prefix)
   uint32_t off_pref;                // stream-K ragged: byte offset of the prefix array in smem
   int32_t trace;                    // dev: record per-CTA start/end/SM into g_trace
-  int32_t sk_qs;                    // stream-K: static items per worker (ranges [P*qs, (P+1)*qs))
+  int32_t sk_static;                // stream-K: cost units split statically (worker P: [B(P), B(P+1)))
   int32_t sk_c;                     // stream-K: items per dynamic tail chunk
   int32_t sk_nchunks;               // stream-K: dynamic tail chunks (0 = static only)
   int32_t sk_total;                 // stream-K: total items
   int* sk_ctr;                      // stream-K: [0] next tail chunk, [1] workers done (zero between calls)
   int32_t sk_np;                    // stream-K: workers (warp pairs) = 4 * grid
+  int32_t sk_cs, sk_cw;             // stream-K cost model: per-unit start cost, cost per window block
   int* sk_pref;                     // stream-K ragged: per-unit item prefix in the workspace (U+1)
   void* out;
   int out_f16;
@@ -960,9 +961,9 @@ __device__ __forceinline__ void store_pairs(uint8_t* smem, const RawRegs<NCH>& r
 // blocks (ceil(n_comp/16)) followed by its window row blocks (ceil(W/16)); the units' item
 // lists are concatenated (N items). A worker is one K/V warp pair (K-warp w, V-warp w+4) and
 // NP = 4 * gridDim.x workers run independently (no CTA-wide sync after the prologue):
-//   static part: worker P takes items [P*qs, (P+1)*qs), which may cross unit boundaries;
-//     its segment (P, u) writes partial slot P + u.
-//   dynamic tail: items [NP*qs, N) in chunks of sk_c items; a worker that runs out of work
+//   static part: worker P takes items [B(P), B(P+1)), B(P) = floor(P*S/NP), which may cross
+//     unit boundaries; its segment (P, u) writes partial slot P + u.
+//   dynamic tail: items [S, N) in chunks of sk_c items; a worker that runs out of work
 //     grabs the next chunk from an atomic counter (equal-work workers run at data-dependent
 //     speeds, measured with tools/trace_ctas.py, so a purely static split ends with its
 //     slowest worker); segment (k, u) of chunk k writes slot NP + U + k + u.
@@ -975,8 +976,8 @@ __device__ __forceinline__ void store_pairs(uint8_t* smem, const RawRegs<NCH>& r
 // segment; the V-warp consumes descriptors in order. Each warp writes its half of the
 // partial (K: m, l per head; V: o per head) when it leaves a segment.
 
-// Dev-only CTA timeline (MSTF_TRACE=1): per CTA {start ns, end ns, smid, nseg, (seg end,
-// after ticket/combine) x 10} recorded by warp pair 0.
+// Dev-only CTA timeline (MSTF_TRACE=1): per CTA {start ns, -, smid, -, K-warp end ns [4],
+// V-warp end ns [4], segments per worker [4], ...}.
 constexpr int kTraceMax = 4096;
 constexpr int kTraceW = 24;
 __device__ unsigned long long g_trace[kTraceW * kTraceMax];
@@ -997,6 +998,27 @@ __device__ __forceinline__ int unit_start(const AttnParams& p, const uint8_t* sm
   return p.sk_nb ? u * p.sk_nb : reinterpret_cast<const int*>(smem + p.off_pref)[u];
 }
 
+// Cost model of the stream-K partition: a unit's cost list is [sk_cs start units (no item:
+// q reload and pipeline restart)][one unit per compressed block][sk_cw units per window
+// block (dense rows, read without software pipelining)]. Workers split the concatenated
+// cost lists evenly; an item belongs to the worker whose range holds its first cost unit.
+__device__ __forceinline__ int unit_cost(const AttnParams& p, int n_comp, int nwb) {
+  return p.sk_cs + (n_comp + 15) / 16 + nwb * p.sk_cw;
+}
+// Index of the first item whose first cost unit is >= x (x unit-relative).
+__device__ __forceinline__ int item_of_cost(const AttnParams& p, int x, int nbc, int nwb) {
+  const int y = x - p.sk_cs;
+  if (y <= 0) return 0;
+  if (y <= nbc) return y;
+  return min(nbc + (y - nbc + p.sk_cw - 1) / p.sk_cw, nbc + nwb);
+}
+
+// Fire-and-forget bulk prefetch into L2 (the window rows of a unit, read after its
+// compressed blocks without software pipelining).
+__device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
 // Unit containing item `it`.
 __device__ __forceinline__ int unit_of_item(const AttnParams& p, const uint8_t* smem, int it) {
   if (p.sk_nb) return it / p.sk_nb;
@@ -1008,14 +1030,23 @@ __device__ __forceinline__ int unit_of_item(const AttnParams& p, const uint8_t* 
   return lo;
 }
 
-// Partial slots of unit u (first item us, end item ue): static workers, then tail chunks,
+// Static partition: worker P owns cost units [B(P), B(P+1)), B(P) = floor(P * S / NP), so
+// every worker gets floor or ceil of S / NP; the owner of unit x is floor(((x+1)*NP - 1) / S).
+__device__ __forceinline__ int worker_begin(const AttnParams& p, int P) {
+  return (int)((long long)P * p.sk_static / p.sk_np);
+}
+__device__ __forceinline__ int worker_of(const AttnParams& p, int x) {
+  return (int)(((long long)(x + 1) * p.sk_np - 1) / p.sk_static);
+}
+
+// Partial slots of unit u (first cost unit us, end ue): static workers, then tail chunks,
 // overlapping it.
 __device__ __forceinline__ PartRanges unit_parts(const AttnParams& p, int u, int us, int ue) {
   const int NP = p.sk_np;
-  const int s_end = min(NP * p.sk_qs, p.sk_total);
+  const int s_end = p.sk_static;
   PartRanges r{0, 0, 0, 0};
   if (us < s_end) {
-    const int cf = us / p.sk_qs, cl = (min(ue, s_end) - 1) / p.sk_qs;
+    const int cf = worker_of(p, us), cl = worker_of(p, min(ue, s_end) - 1);
     r.b1 = cf + u;
     r.n1 = cl - cf + 1;
   }
@@ -1045,7 +1076,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
   if (tracing && threadIdx.x == 0) {
     g_trace[kTraceW * cta] = global_ns();
     g_trace[kTraceW * cta + 2] = smid();
-    g_trace[kTraceW * cta + 3] = 0;
+    for (int i = 3; i < kTraceW; ++i) g_trace[kTraceW * cta + i] = 0;
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < 32; ++i) mbar_init(&hfull[i], 1);
@@ -1060,7 +1091,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
     int carry = 0;
     for (int u0 = 0; u0 < c.U; u0 += 32) {
       const int uu = u0 + lane;
-      const int items = uu < c.U ? (c.n_comp[uu] + 15) / 16 + nwb : 0;
+      const int items = uu < c.U ? unit_cost(p, c.n_comp[uu], nwb) : 0;
       int incl = items;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1095,11 +1126,12 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
     // [6] prefetched tail chunk, [7] more work, [8] unit end (absolute).
     __shared__ int s_seg[4][10];
     volatile int* sg = s_seg[w];
-    auto set_bounds = [&]() {  // lane 0
+    auto set_bounds = [&]() {  // lane 0: cost range of the segment -> item range [lo, hi)
       const int u0 = sg[0];
       const int us = unit_start(p, smem, u0), ue = unit_start(p, smem, u0 + 1);
-      sg[3] = sg[1] - us;
-      sg[4] = min((int)sg[2], ue) - us;
+      const int nbc0 = (c.n_comp[u0] + 15) / 16;
+      sg[3] = item_of_cost(p, sg[1] - us, nbc0, nwb);
+      sg[4] = item_of_cost(p, min((int)sg[2], ue) - us, nbc0, nwb);
       sg[8] = ue;
     };
     auto publish = [&](int4 d) {  // lane 0: descriptor for the V-warp
@@ -1110,11 +1142,11 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
     };
     if (lane == 0) {
       const int P = (int)blockIdx.x * 4 + w;
-      const int it0 = P * p.sk_qs;
-      sg[7] = it0 < p.sk_total;
+      const int it0 = worker_begin(p, P), it1 = worker_begin(p, P + 1);
+      sg[7] = it0 < it1;
       if (sg[7]) {
         sg[1] = it0;
-        sg[2] = min(it0 + p.sk_qs, p.sk_total);
+        sg[2] = it1;
         sg[0] = unit_of_item(p, smem, it0);
         sg[5] = P;
         set_bounds();
@@ -1134,6 +1166,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
       const int n = c.n_comp[u];
       const int nbc = (n + 15) / 16;
       const int bbeg = min((int)sg[3], nbc), bend = min((int)sg[4], nbc);
+      if (lane == 0 && (int)sg[4] > nbc) l2_prefetch(c.win[0] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
       st.m0 = st.m1 = -INFINITY;
       st.l0 = st.l1 = 0.f;
       if (u != qu) {
@@ -1235,14 +1268,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
       }
       __syncwarp();
       if (lane == 0) {
-        if (tracing && w == 0) {
-          const int ns = (int)g_trace[kTraceW * cta + 3];
-          if (ns < 10) {
-            g_trace[kTraceW * cta + 4 + 2 * ns] = global_ns();
-            g_trace[kTraceW * cta + 5 + 2 * ns] = u;
-            g_trace[kTraceW * cta + 3] = ns + 1;
-          }
-        }
+        if (tracing) g_trace[kTraceW * cta + 12 + w] += 1;  // segments of worker w
         // advance: rest of the range in the next unit, else the next tail chunk, else done
         if (sg[2] > sg[8]) {
           sg[1] = sg[8];
@@ -1250,7 +1276,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
           set_bounds();
         } else if (p.sk_nchunks > 0 && sg[6] < p.sk_nchunks) {
           const int k = sg[6];
-          const int it0 = min(NP * p.sk_qs, p.sk_total) + k * p.sk_c;
+          const int it0 = p.sk_static + k * p.sk_c;
           sg[1] = it0;
           sg[2] = min(it0 + p.sk_c, p.sk_total);
           sg[0] = unit_of_item(p, smem, it0);
@@ -1268,7 +1294,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
       }
       __syncwarp();
     }
-    if (tracing && w == 0 && lane == 0) g_trace[kTraceW * cta + 1] = global_ns();
+    if (tracing && lane == 0) g_trace[kTraceW * cta + 4 + w] = global_ns();  // K-warp w done
   } else {
     // ================= V-warp: P.V over the segments the K-warp publishes
     for (;;) {
@@ -1279,10 +1305,14 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
       if (lane == 0) mbar_arrive(&dempty[2 * w + ds]);
       ++nseg;
       const int u = d.x;
-      if (u < 0) break;
+      if (u < 0) {
+        if (tracing && lane == 0) g_trace[kTraceW * cta + 8 + w] = global_ns();  // V-warp w done
+        break;
+      }
       const int n = c.n_comp[u];
       const int nbc = (n + 15) / 16;
       const int bbeg = min(d.y, nbc), bend = min(d.z, nbc);
+      if (lane == 0 && d.z > nbc) l2_prefetch(c.win[1] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
       float acc[2][4][4];
 #pragma unroll
       for (int e = 0; e < 2; ++e)
@@ -1546,7 +1576,20 @@ static int32_t pair_region_bytes(int32_t kp, bool v) {
   return (b + 127) / 128 * 128;
 }
 
-// Register-staged kernel (fused combine, stream-K) for equal K/V k_pad of 16, 32 or 40;
+void sk_cost_params(int32_t* cs, int32_t* cw) {
+  static const int32_t s_cs = std::getenv("MSTF_SKCS") ? std::atoi(std::getenv("MSTF_SKCS")) : 2;
+  static const int32_t s_cw = std::getenv("MSTF_SKCW") ? std::max(1, std::atoi(std::getenv("MSTF_SKCW"))) : 2;
+  *cs = s_cs;
+  *cw = s_cw;
+}
+
+int32_t sk_unit_cost(int32_t n_comp, int32_t W) {
+  int32_t cs, cw;
+  sk_cost_params(&cs, &cw);
+  return cs + (n_comp + 15) / 16 + (W > 0 ? (W + 15) / 16 : 0) * cw;
+}
+
+// Register-staged kernel (stream-K + combine kernel) for equal K/V k_pad of 16, 32 or 40;
 // the TMA-staged kernel + separate combine otherwise.
 bool uses_reg_kernel(int32_t kpad_k, int32_t kpad_v) {
   const int32_t nk = kpad_k / 8;
@@ -1583,7 +1626,7 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
   // (<= kSkChunksPerWorker per worker). Ragged units need a (U+1)-int prefix array in shared
   // memory, so very large ragged U falls back to the TMA kernel's split grid.
   pl.sk = 0;
-  pl.sk_qs = pl.sk_nb = pl.sk_grid = pl.sk_c = pl.sk_nchunks = 0;
+  pl.sk_static = pl.sk_nb = pl.sk_grid = pl.sk_c = pl.sk_nchunks = 0;
   pl.sk_total = 0;
   if (uses_reg_kernel(kpad_k, kpad_v) && total_items > 0 && total_items < (1ll << 30) &&
       (uniform_items > 0 || U <= kMaxSkPrefix)) {
@@ -1597,16 +1640,16 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
     if (const char* e = std::getenv("MSTF_SKTAIL")) tail_pct = std::atoi(e);  // tuning override
     int64_t min_chunk = 2;
     if (const char* e = std::getenv("MSTF_SKC")) min_chunk = std::max<int64_t>(1, std::atoi(e));
-    const int64_t q = (total_items + np - 1) / np;
-    int64_t qs = q, chunk = 0, nchunks = 0;
+    const int64_t q = total_items / np;
+    int64_t stat = total_items, chunk = 0, nchunks = 0;
     if (tail_pct > 0 && q >= 8) {
-      qs = total_items * (100 - tail_pct) / (100 * np);
-      const int64_t tail = total_items - np * qs;
+      stat = total_items * (100 - tail_pct) / 100;
+      const int64_t tail = total_items - stat;
       chunk = std::max(min_chunk, (tail + kSkChunksPerWorker * np - 1) / (kSkChunksPerWorker * np));
       nchunks = (tail + chunk - 1) / chunk;
     }
     pl.sk = 1;
-    pl.sk_qs = (int32_t)qs;
+    pl.sk_static = (int32_t)stat;
     pl.sk_grid = (int32_t)grid;
     pl.sk_c = (int32_t)chunk;
     pl.sk_nchunks = (int32_t)nchunks;
@@ -1642,7 +1685,7 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.out = out;
   p.out_f16 = out_f16;
   p.sk = 0;
-  p.sk_qs = p.sk_nb = p.sk_c = p.sk_nchunks = p.sk_total = 0;
+  p.sk_static = p.sk_nb = p.sk_c = p.sk_nchunks = p.sk_total = 0;
   p.sk_ctr = p.tickets + c.U;
   p.sk_pref = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ((size_t)(c.U + 2) * sizeof(int) + 255) / 256 * 256);
   p.sk_np = 0;
@@ -1672,12 +1715,13 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
     pr.off_pairs = kBarBytesReg + kHandoffBytes;
     int rsmem = pr.off_pairs + plan.pair_bytes;
     pr.sk = 1;
-    pr.sk_qs = plan.sk_qs;
+    pr.sk_static = plan.sk_static;
     pr.sk_c = plan.sk_c;
     pr.sk_nchunks = plan.sk_nchunks;
     pr.sk_total = plan.sk_total;
     pr.sk_nb = plan.sk_nb;
     pr.sk_np = 4 * plan.sk_grid;
+    sk_cost_params(&pr.sk_cs, &pr.sk_cw);
     pr.off_pref = (uint32_t)rsmem;
     if (plan.sk_nb == 0) rsmem += (c.U + 1) * (int)sizeof(int);
     const dim3 grid(plan.sk_grid, 1);

@@ -66,18 +66,21 @@ struct AttnPlan {
   int32_t pair_bytes;    // per-CTA shifted pair arrays (4 warps x 16 tokens x K,V)
   int32_t reg_k, reg_v;  // per-warp region bytes
   int32_t sk;            // 1: stream-K schedule (register-staged kernel)
-  int32_t sk_qs;         // static items (16-token blocks) per worker (warp pair)
+  int32_t sk_static;     // cost units split statically over the workers (warp pairs)
   int32_t sk_c;          // items per dynamic tail chunk
   int32_t sk_nchunks;    // dynamic tail chunks
   int32_t sk_total;      // total items
   int32_t sk_nb;         // items per unit when all units are equal, else 0
   int32_t sk_grid;       // CTAs
 };
-// total_items = sum over units of ceil(n_comp/16) + ceil(W/16); uniform_items = that per-unit count
+// total_items = sum over units of sk_unit_cost(n_comp, W); uniform_items = that per-unit cost
 // when it is the same for every unit, else 0.
 AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_t uniform_items,
                         int32_t kpad_k, int32_t kpad_v, int32_t sm_count);
 bool uses_reg_kernel(int32_t kpad_k, int32_t kpad_v);
+// Stream-K partition cost of one unit (see unit_cost in attention.cu) and its parameters.
+int32_t sk_unit_cost(int32_t n_comp, int32_t W);
+void sk_cost_params(int32_t* cs, int32_t* cw);
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits);
 int32_t max_splits_for(int32_t U, int32_t capacity);
 

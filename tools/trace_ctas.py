@@ -1,5 +1,5 @@
-"""Per-CTA / per-segment timeline of one attention launch (dev tool, GPU; sets MSTF_TRACE).
-Record per CTA: start, end, smid, nseg, then (segment body end, after combine) pairs."""
+"""Per-worker timeline of one attention launch (dev tool, GPU; sets MSTF_TRACE): when each
+K/V warp pair finishes, relative to the kernel start."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth
@@ -21,24 +21,16 @@ def trace(Bt=16, T=4096, keep=39, hkv=8, hq=32):
     a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, TW).astype(np.int64)
     a = a[a[:, 0] > 0]
     t0 = a[:, 0].min()
-    st, en = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3
-    nseg = a[:, 3]
-    print(f"{os.environ.get('TAG','')} CTAs {len(a)} span {en.max():.1f} us; end p0/p50/max {en.min():.1f}/{np.median(en):.1f}/{en.max():.1f}; "
-          f"segments per CTA {np.bincount(nseg).tolist()}", flush=True)
-    # per-segment: body duration and combine duration
-    body, comb = [], []
-    for r in a:
-        prev = r[0]
-        for i in range(int(r[3])):
-            te, tc = r[4 + 2 * i], r[5 + 2 * i]
-            body.append((te - prev) / 1e3); comb.append((tc - te) / 1e3); prev = tc
-    body, comb = np.array(body), np.array(comb)
-    print(f"   segment body p50/p90/max {np.median(body):.1f}/{np.percentile(body,90):.1f}/{body.max():.1f} us; "
-          f"combine+ticket p50/p90/max {np.median(comb):.2f}/{np.percentile(comb,90):.2f}/{comb.max():.2f} us", flush=True)
-    # first 3 CTAs in detail
-    for r in a[:3]:
-        segs = [((r[4 + 2 * i] - t0) / 1e3, (r[5 + 2 * i] - t0) / 1e3) for i in range(int(r[3]))]
-        print("   cta", [(round(x, 1), round(y, 1)) for x, y in segs], flush=True)
+    ke = (a[:, 4:8] - t0).ravel() / 1e3
+    ve = (a[:, 8:12] - t0).ravel() / 1e3
+    segs = a[:, 12:16].ravel()
+    pc = lambda x: "/".join(f"{np.percentile(x, q):.1f}" for q in (0, 10, 50, 90, 100))
+    print(f"{os.environ.get('TAG','')} workers {len(ve)}: K end p0/10/50/90/100 {pc(ke)}; V end {pc(ve)} us; "
+          f"V-K lag p50 {np.median(ve - ke):.1f}; segments {np.bincount(segs).tolist()}", flush=True)
+    # slow workers: by segments
+    for s_ in np.unique(segs):
+        print(f"   {s_} segments: V end mean {ve[segs == s_].mean():.1f} us (n={int((segs == s_).sum())})")
+    np.save("gpurun_out/worker_ends.npy", np.stack([ke, ve, segs]))
 
 os.environ["MSTF_TRACE"] = "1"
 trace()
