@@ -10,7 +10,7 @@ for w in C2_s50 C3 C4 C5; do
   timeout 600 python bench.py --steps 5 --warmup 3 --workload $w --no-cpu-baseline > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
 done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:mstf --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"mstf_|append_kernel|prefill_kernel|set_counters" --csv \
    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-dense --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mstf_attn -s 40 -c 1 \
    -o gpurun_out/prof_bench python bench.py --steps 2 --warmup 3 --no-dense --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
