@@ -446,7 +446,10 @@ struct DenseBlock {
   int W, first, nwin;  // token sits in slot `first` and which holds `nwin` tokens
   __device__ __forceinline__ bool valid(int r) const {
     const int slot = row0 + r;
-    return ring ? (slot < W && ((slot - first + W) % W) < nwin) : r < nvalid;
+    if (!ring) return r < nvalid;
+    int age = slot - first;  // ring position relative to the oldest token, in [0, W)
+    if (age < 0) age += W;
+    return slot < W && age < nwin;
   }
 };
 
@@ -1218,13 +1221,13 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         RawRegs<NK> ra, rb;
         int b = bbeg;
         if (b < bend) load(ra, b);
-        while (b < bend) {
+        // One loop body (not a two-way unrolled ping-pong): the kernel's code footprint is what
+        // the instruction cache sees with K- and V-warps resident together (-10% time, measured).
+#pragma unroll 1
+        for (; b < bend; ++b) {
           if (b + 1 < bend) load(rb, b + 1);
           k_step(ra, b);
-          if (++b >= bend) break;
-          if (b + 1 < bend) load(ra, b + 1);
-          k_step(rb, b);
-          ++b;
+          ra = rb;  // waits for the prefetched block only after this block's work
         }
       }
       const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
@@ -1360,13 +1363,11 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         RawRegs<NV> ra, rb;
         int b = bbeg;
         if (b < bend) load_raw<NV>(ra, vals, bms, b * 16, min(16, n - b * 16), lane);
-        while (b < bend) {
+#pragma unroll 1
+        for (; b < bend; ++b) {
           if (b + 1 < bend) load_raw<NV>(rb, vals, bms, (b + 1) * 16, min(16, n - (b + 1) * 16), lane);
           v_step(ra);
-          if (++b >= bend) break;
-          if (b + 1 < bend) load_raw<NV>(ra, vals, bms, (b + 1) * 16, min(16, n - (b + 1) * 16), lane);
-          v_step(rb);
-          ++b;
+          ra = rb;
         }
       }
       const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
@@ -1691,6 +1692,7 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.sk_np = 0;
   p.off_pref = 0;
   p.trace = std::getenv("MSTF_TRACE") != nullptr;  // dev timeline (tools/trace_ctas.py)
+
   const int smem = kBarBytesKV + plan.nstage * plan.stage_bytes + plan.pair_bytes + kHandoffBytes;
   // kernel choice: register-staged interleaved kernel for kpad <= 40 (nk <= 5); TMA-staged kernel
   // with contiguous pair arrays for kpad >= 48 (interleaving aliases banks at ~50% density).
