@@ -385,6 +385,26 @@ __device__ __forceinline__ void gather8_s(const uint8_t* smem, uint32_t hw, uint
 #undef MSTF_G
 }
 
+// Interleaved V gather (register-staged kernel): the two lanes that share a bitmap word take
+// alternating dibits rather than its two 16-bit halves, so in one gather instruction they read
+// adjacent pair-array rows (fewer shared-memory bank conflicts; same instruction count).
+// V: the lane pair (2w', 2w'+1) of a token shares bitmap word wv; lane parity h takes its
+// dibits 2i + h (channels 32w' + 4i + 2h, +1), i = 0..7. base = absolute smem address of pair
+// entry (kept values before word wv).
+template <int STRIDE>
+__device__ __forceinline__ void gather8_il(uint32_t wv, uint32_t base, int h, uint32_t (&out)[8]) {
+  // bits p = 4i + 2h, p + 1 sit in byte i/2 at bit 4(i&1) + 2h
+  const uint32_t ce0 = wv << (7 - 2 * h), ce1 = wv << (6 - 2 * h);  // i even
+  const uint32_t co0 = wv << (3 - 2 * h), co1 = wv << (2 - 2 * h);  // i odd
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t m = i >> 1;
+    const uint32_t sel = (8u | m) | ((8u | m) << 4) | ((12u | m) << 8) | ((12u | m) << 12);
+    const uint32_t pc = __popc(wv << (31 - 4 * i - 2 * h));  // kept channels <= 4i + 2h
+    out[i] = lds_abs_masked(base + STRIDE * pc, (i & 1) ? prmt(co0, co1, sel) : prmt(ce0, ce1, sel));
+  }
+}
+
 template <int NK>
 __device__ __forceinline__ void fill_k3(const CompBlock& cb, uint8_t* smem, uint32_t (&kr)[2][16], int lane) {
   const int g = lane >> 2, t = lane & 3;
@@ -1342,7 +1362,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         }
         const uint32_t ev = iv - pv;
         __syncwarp();
-        const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
+        const int sa = 8 * t + (g >> 1), sb = sa + 4;
         const uint32_t w2t = __shfl_sync(0xffffffffu, cur.bm0, sa), w2t8 = __shfl_sync(0xffffffffu, cur.bm1, sa);
         const uint32_t w2t1 = __shfl_sync(0xffffffffu, cur.bm0, sb), w2t9 = __shfl_sync(0xffffffffu, cur.bm1, sb);
         const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
@@ -1351,21 +1371,23 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         uint32_t vr[4][8];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
-          const uint32_t base = ybase + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * (ps[x] + extra);
-          gather8_s<16>(smem, ws[x] >> hsh, base, vr[x]);
+          const uint32_t base = smem_u32(smem) + ybase + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * ps[x];
+          gather8_il<16>(ws[x], opaque(base), g & 1, vr[x]);
         }
         v_block(vr, handoff_get(), acc);
       };
       {
-        const uint16_t* vals = c.val[1] + (size_t)u * c.cap * c.kpad[1];
-        const uint64_t* bms = c.bm[1] + (size_t)u * c.cap * kTiles;
+        // unit base pointers are re-derived per load (saves registers in the hot loop)
+        auto load = [&](RawRegs<NV>& rr, int bb) {
+          const size_t ub = (size_t)u * c.cap;
+          load_raw<NV>(rr, c.val[1] + ub * c.kpad[1], c.bm[1] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
+        };
         RawRegs<NV> ra, rb;
         int b = bbeg;
-        if (b < bend) load_raw<NV>(ra, vals, bms, b * 16, min(16, n - b * 16), lane);
+        if (b < bend) load(ra, b);
 #pragma unroll 1
         for (; b < bend; ++b) {
-          if (b + 1 < bend) load_raw<NV>(rb, vals, bms, (b + 1) * 16, min(16, n - (b + 1) * 16), lane);
+          if (b + 1 < bend) load(rb, b + 1);
           v_step(ra);
           ra = rb;
         }
@@ -1384,11 +1406,11 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
 #pragma unroll
         for (int x4 = 0; x4 < 4; ++x4) {
-          if (db.valid(tk[x4])) {
-            const uint4* pp = reinterpret_cast<const uint4*>(db.v + (size_t)(db.row0 + tk[x4]) * kD + 16 * g);
-            const uint4 a4 = pp[0], bb = pp[1];
-            vr[x4][0] = a4.x; vr[x4][1] = a4.y; vr[x4][2] = a4.z; vr[x4][3] = a4.w;
-            vr[x4][4] = bb.x; vr[x4][5] = bb.y; vr[x4][6] = bb.z; vr[x4][7] = bb.w;
+          if (db.valid(tk[x4])) {  // interleaved channel order (see gather8_il)
+            const uint32_t* pp = reinterpret_cast<const uint32_t*>(db.v + (size_t)(db.row0 + tk[x4]) * kD) +
+                                 16 * (g >> 1) + (g & 1);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) vr[x4][j] = pp[2 * j];
           } else {
 #pragma unroll
             for (int j = 0; j < 8; ++j) vr[x4][j] = 0;
@@ -1397,15 +1419,16 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         v_block(vr, handoff_get(), acc);
       }
       float* o = p.ws_o + (size_t)d.w * p.G * kD;
+      // m-tile i, row g <-> channels 32(g>>1) + 4i + 2(g&1) (+1: odd accumulator); row g+8: +16
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int h = 2 * t + hh;
         if (h < p.G) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            *reinterpret_cast<float2*>(o + h * kD + 16 * g + 2 * i) = make_float2(acc[0][i][hh], acc[1][i][hh]);
-            *reinterpret_cast<float2*>(o + h * kD + 16 * g + 8 + 2 * i) =
-                make_float2(acc[0][i][2 + hh], acc[1][i][2 + hh]);
+            const int ch = 32 * (g >> 1) + 4 * i + 2 * (g & 1);
+            *reinterpret_cast<float2*>(o + h * kD + ch) = make_float2(acc[0][i][hh], acc[1][i][hh]);
+            *reinterpret_cast<float2*>(o + h * kD + ch + 16) = make_float2(acc[0][i][2 + hh], acc[1][i][2 + hh]);
           }
         }
       }
