@@ -701,6 +701,8 @@ __global__ void __launch_bounds__(kThreadsKV, 2) mstf_attn_kv_kernel(const AttnP
   const int u = blockIdx.y, split = blockIdx.x, S = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const CacheView& c = p.c;
+  pdl_launch_dependents();
+  pdl_wait();  // cache, counters and q may be written by the previous kernel in the stream
   const int n = c.n_comp[u];
   const int chunks_total = (n + kChunk - 1) / kChunk;
   const int cps = (chunks_total + S - 1) / S;
@@ -1497,6 +1499,8 @@ __global__ void __launch_bounds__(kMaxGroup * 32) mstf_sk_combine_kernel(const A
 // ---------------------------------------------------------------- K3: combine partials
 __global__ void mstf_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int nparts,
                                     int G, void* out, int out_f16) {
+  pdl_launch_dependents();
+  pdl_wait();  // partials come from the attention kernel just before
   // one warp per (unit, head); lane owns channels 4*lane .. 4*lane+3
   const int u = blockIdx.x, h = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (h >= G) return;
@@ -1758,11 +1762,10 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(plan.splits, c.U), kThreadsKV, smem, s>>>(p);
-  e = cudaGetLastError();
+  e = launch_pdl(kern, dim3(plan.splits, c.U), dim3(kThreadsKV), (size_t)smem, s, p);
   if (e != cudaSuccess) return e;
-  mstf_combine_kernel<<<c.U, G * 32, 0, s>>>(p.ws_o, p.ws_ml, plan.splits * kConsumerWarps, G, out, out_f16);
-  return cudaGetLastError();
+  return launch_pdl(mstf_combine_kernel, dim3(c.U), dim3(G * 32), 0, s, (const float*)p.ws_o, (const float*)p.ws_ml,
+                    (int)(plan.splits * kConsumerWarps), (int)G, out, (int)out_f16);
 }
 
 cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const int32_t* lengths, int32_t U,
