@@ -170,6 +170,21 @@ int mstf_dense_decode_attention(const void* k, const void* v, const int32_t* len
  * slices are contiguous in [B][Hq][d]. Host-only.                                      */
 int mstf_shard_units(int32_t units, int32_t world, int32_t rank, int32_t* u0, int32_t* u1);
 
+/* One decode step of a layer: exactly mstf_append_token(k_new, v_new) followed by
+ * mstf_sparse_decode_attention(q, ...) (R12: the new token attends to itself), with the same
+ * arguments, layouts, results and errors. P:234 (compress on exit from the window) + Alg. 1.
+ * When every unit has the same counters and k_pad selects the register-staged kernel, the
+ * append runs inside the attention launch (one kernel + the split combine instead of three
+ * launches); otherwise the two calls are made in sequence. The workspace must come from
+ * mstf_workspace_bytes, be zero-filled once before first use (it carries per-unit ready flags
+ * stamped per call), and not be shared by calls that may run concurrently. */
+int mstf_decode_step(mstf_cache* cache, const void* k_new, const void* v_new, const void* q, float scale,
+                     void* out, int32_t out_dtype, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Kernels one mstf_decode_step call on this cache (in its current state) launches: 2 fused,
+ * 3 unfused; negative status for a NULL handle. Host-only. */
+int mstf_decode_step_kernel_count(const mstf_cache* cache);
+
 /* Number of kernels one mstf_sparse_decode_attention call on this cache launches (the
  * attention kernel and the split combine), or a negative status for a NULL handle.
  * Host-only; lets callers count launches. */

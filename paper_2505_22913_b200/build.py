@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libmustafar.so")
 SOURCES = ["abi.cu", "compress.cu", "attention.cu"]
-HEADERS = ["kernels.cuh", "ptx.cuh"]
+HEADERS = ["kernels.cuh", "ptx.cuh", "compress_dev.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

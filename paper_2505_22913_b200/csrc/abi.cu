@@ -1,6 +1,7 @@
 // abi.cu -- the extern "C" boundary declared in include/mustafar.h: host-side validation,
 // buffer sizing, the exact host mirror of the per-unit counters, and kernel launches.
 // No device allocation, no synchronisation.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -160,36 +161,113 @@ size_t mstf_workspace_bytes(const mstf_cache* h) {
   return attention_ws_bytes(h->view.U, h->cfg.num_q_heads / h->cfg.num_kv_heads, h->max_splits);
 }
 
-int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale, void* out, int32_t out_dtype,
-                                 void* ws, size_t ws_bytes, void* stream) {
-  if (!h || !q || !out || !aligned16(q)) return MSTF_EINVAL;
-  if (out_dtype != MSTF_OUT_F32 && out_dtype != MSTF_OUT_F16) return MSTF_EINVAL;
-  if (!ws || !aligned16(ws) || ws_bytes < mstf_workspace_bytes(h)) return MSTF_EWORKSPACE;
+namespace {
+// Attention plan from the host mirror (counters as they will be when the kernels run).
+int make_plan(const mstf_cache* h, const std::vector<int32_t>& nc, const std::vector<int32_t>& nw, AttnPlan* plan) {
   int32_t max_comp = 0;
   int64_t total_items = 0;
-  int32_t uniform_items = sk_unit_cost(h->nc[0], h->view.W);
+  int32_t uniform_items = sk_unit_cost(nc[0], h->view.W);
   for (int32_t u = 0; u < h->view.U; ++u) {
-    if (h->nc[u] + h->nw[u] == 0) return MSTF_EEMPTY;
-    if (h->nc[u] > max_comp) max_comp = h->nc[u];
-    const int32_t items = sk_unit_cost(h->nc[u], h->view.W);
+    if (nc[u] + nw[u] == 0) return MSTF_EEMPTY;
+    if (nc[u] > max_comp) max_comp = nc[u];
+    const int32_t items = sk_unit_cost(nc[u], h->view.W);
     total_items += items;
     if (items != uniform_items) uniform_items = 0;
   }
-  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
-  AttnPlan plan = plan_attention(h->view.U, max_comp, total_items, uniform_items, h->view.kpad[0],
-                                 h->view.kpad[1], sm_count());
+  *plan = plan_attention(h->view.U, max_comp, total_items, uniform_items, h->view.kpad[0], h->view.kpad[1],
+                         sm_count());
   if (const char* env = std::getenv("MSTF_SCHED")) {  // tuning override: "split" forces the split grid
-    if (std::strcmp(env, "split") == 0) plan.sk = 0;
+    if (std::strcmp(env, "split") == 0) plan->sk = 0;
   }
   if (const char* env = std::getenv("MSTF_SPLITS")) {  // tuning override (not part of the ABI contract)
     const int v = std::atoi(env);
-    if (v > 0) plan.splits = v;
+    if (v > 0) plan->splits = v;
   }
-  if (plan.splits > h->max_splits) plan.splits = h->max_splits;
+  if (plan->splits > h->max_splits) plan->splits = h->max_splits;
+  return MSTF_OK;
+}
+
+int check_attention_args(const mstf_cache* h, const void* q, const void* out, int32_t out_dtype, const void* ws,
+                         size_t ws_bytes) {
+  if (!h || !q || !out || !aligned16(q)) return MSTF_EINVAL;
+  if (out_dtype != MSTF_OUT_F32 && out_dtype != MSTF_OUT_F16) return MSTF_EINVAL;
+  if (!ws || !aligned16(ws) || ws_bytes < mstf_workspace_bytes(h)) return MSTF_EWORKSPACE;
+  return MSTF_OK;
+}
+
+// Stamp of a fused step's ready flags: unique across calls and caches of the process.
+int32_t next_epoch() {
+  static std::atomic<int32_t> e{0};
+  int32_t v = ++e;
+  if (v <= 0) {  // wrapped after 2^31 calls
+    e = 1;
+    v = 1;
+  }
+  return v;
+}
+}  // namespace
+
+int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale, void* out, int32_t out_dtype,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  const int st = check_attention_args(h, q, out, out_dtype, ws, ws_bytes);
+  if (st != MSTF_OK) return st;
+  AttnPlan plan;
+  const int sp = make_plan(h, h->nc, h->nw, &plan);
+  if (sp != MSTF_OK) return sp;
+  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
   if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, out,
                               out_dtype == MSTF_OUT_F16, ws, static_cast<cudaStream_t>(stream)) != cudaSuccess)
     return MSTF_ECUDA;
   return MSTF_OK;
+}
+
+int mstf_decode_step(mstf_cache* h, const void* k_new, const void* v_new, const void* q, float scale, void* out,
+                     int32_t out_dtype, void* ws, size_t ws_bytes, void* stream) {
+  if (!h || !k_new || !v_new || !aligned16(k_new) || !aligned16(v_new)) return MSTF_EINVAL;
+  const int st = check_attention_args(h, q, out, out_dtype, ws, ws_bytes);
+  if (st != MSTF_OK) return st;
+  const int32_t U = h->view.U, W = h->view.W;
+  for (int32_t u = 0; u < U; ++u)
+    if ((W == 0 || h->nw[u] == W) && h->nc[u] + 1 > h->view.cap) return MSTF_ECAPACITY;
+  // counters after the append (a4)
+  std::vector<int32_t> nc = h->nc, nw = h->nw;
+  bool uniform = true;
+  for (int32_t u = 0; u < U; ++u) {
+    uniform = uniform && nc[u] == nc[0] && nw[u] == nw[0];
+    if (W == 0 || nw[u] == W) nc[u] += 1; else nw[u] += 1;
+  }
+  AttnPlan plan;
+  const int sp = make_plan(h, nc, nw, &plan);
+  if (sp != MSTF_OK) return sp;
+  if (!uniform || !plan.sk) {  // ragged cache or TMA kernel: the two launches in sequence
+    const int sa = mstf_append_token(h, k_new, v_new, stream);
+    if (sa != MSTF_OK) return sa;
+    return mstf_sparse_decode_attention(h, q, scale, out, out_dtype, ws, ws_bytes, stream);
+  }
+  FuseArgs fa;
+  fa.k_new = static_cast<const uint16_t*>(k_new);
+  fa.v_new = static_cast<const uint16_t*>(v_new);
+  fa.nc_old = h->nc[0];
+  fa.nw_old = h->nw[0];
+  fa.unc = nc[0];
+  fa.unw = nw[0];
+  fa.evict = (W == 0 || h->nw[0] == W) ? 1 : 0;
+  fa.epoch = next_epoch();
+  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
+  if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, out,
+                              out_dtype == MSTF_OUT_F16, ws, static_cast<cudaStream_t>(stream), &fa) != cudaSuccess)
+    return MSTF_ECUDA;
+  h->nc = nc;
+  h->nw = nw;
+  return MSTF_OK;
+}
+
+int mstf_decode_step_kernel_count(const mstf_cache* h) {
+  if (!h) return MSTF_EINVAL;
+  bool uniform = true;
+  for (int32_t u = 1; u < h->view.U; ++u) uniform = uniform && h->nc[u] == h->nc[0] && h->nw[u] == h->nw[0];
+  // fused (register kernel + combine) or append + attention + combine
+  return uniform && uses_reg_kernel(h->view.kpad[0], h->view.kpad[1]) ? 2 : 3;
 }
 
 static int32_t dense_splits(int32_t units, int32_t t_max) {

@@ -40,6 +40,7 @@
 #include <cmath>
 #include <cstdlib>
 
+#include "compress_dev.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
 
@@ -70,6 +71,13 @@ struct AttnParams {
   int* sk_ctr;                      // stream-K: [0] next tail chunk, [1] workers done (zero between calls)
   int32_t sk_np;                    // stream-K: workers (warp pairs) = 4 * grid
   int32_t sk_cs, sk_cw;             // stream-K cost model: per-unit start cost, cost per window block
+  // fused decode step (append + attention in one launch; uniform caches): counters before
+  // (nc_old, nw_old) and after (unc, unw) the append, whether a window token was evicted into
+  // record nc_old, the new tokens, and per-unit ready flags [2U] stamped with `epoch`
+  int32_t fuse, evict, nc_old, nw_old, unc, unw, epoch;
+  const uint16_t* k_new;
+  const uint16_t* v_new;
+  int* ready;
   int* sk_pref;                     // stream-K ragged: per-unit item prefix in the workspace (U+1)
   void* out;
   int out_f16;
@@ -943,6 +951,9 @@ struct RawRegs {
   uint32_t bm0, bm1;  // bitmap word t of tokens g, g+8
 };
 
+// Coherent cached loads (ld.global.ca, not the read-only .nc path): in a fused decode step
+// the last block of a unit was written earlier in the same launch, and the acquire in
+// wait_ready must order these loads after it.
 template <int NCH>
 __device__ __forceinline__ void load_raw(RawRegs<NCH>& rr, const uint16_t* __restrict__ vals,
                                          const uint64_t* __restrict__ bms, int tok0, int nvalid, int lane) {
@@ -952,12 +963,13 @@ __device__ __forceinline__ void load_raw(RawRegs<NCH>& rr, const uint16_t* __res
   // words wb .. wb + nw - 1 of token tok0 + tau, wb = m0/2 - 1 (h = 0: word -1 is zero)
   const uint32_t* src = reinterpret_cast<const uint32_t*>(vals + (size_t)(tok0 + tau) * Gm::kp) + (m0 / 2 - 1);
   const bool ok = tau < nvalid;
-  rr.W[0] = (h && ok) ? __ldg(src) : 0u;
+  auto ld = [](const uint32_t* a) { return __ldca(a); };
+  rr.W[0] = (h && ok) ? ld(src) : 0u;
 #pragma unroll
-  for (int i = 1; i < Gm::nw; ++i) rr.W[i] = ok ? __ldg(src + i) : 0u;
+  for (int i = 1; i < Gm::nw; ++i) rr.W[i] = ok ? ld(src + i) : 0u;
   const uint32_t* bw = reinterpret_cast<const uint32_t*>(bms);
-  rr.bm0 = g < nvalid ? __ldg(bw + (size_t)(tok0 + g) * 4 + t) : 0u;
-  rr.bm1 = g + 8 < nvalid ? __ldg(bw + (size_t)(tok0 + g + 8) * 4 + t) : 0u;
+  rr.bm0 = g < nvalid ? ld(bw + (size_t)(tok0 + g) * 4 + t) : 0u;
+  rr.bm1 = g + 8 < nvalid ? ld(bw + (size_t)(tok0 + g + 8) * 4 + t) : 0u;
 }
 
 template <int NCH, bool IS_V>
@@ -1038,6 +1050,25 @@ __device__ __forceinline__ int item_of_cost(const AttnParams& p, int x, int nbc,
   return min(nbc + (y - nbc + p.sk_cw - 1) / p.sk_cw, nbc + nwb);
 }
 
+// Unit counters as the attention sees them: after the append (host mirror) in a fused step,
+// else the device counters.
+__device__ __forceinline__ int ncomp_of(const AttnParams& p, int u) { return p.fuse ? p.unc : p.c.n_comp[u]; }
+__device__ __forceinline__ int nwin_of(const AttnParams& p, int u) { return p.fuse ? p.unw : p.c.n_win[u]; }
+
+// Fused step: wait until the warp that appended this unit's tensor published it.
+__device__ __forceinline__ void wait_ready(const int* flag, int epoch, int lane) {
+  if (lane == 0) {
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    } while (v != epoch);
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void publish_ready(int* flag, int epoch) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
 // Fire-and-forget bulk prefetch into L2 (the window rows of a unit, read after its
 // compressed blocks without software pipelining).
 __device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
@@ -1063,7 +1094,6 @@ __device__ __forceinline__ int worker_begin(const AttnParams& p, int P) {
 __device__ __forceinline__ int worker_of(const AttnParams& p, int x) {
   return (int)(((long long)(x + 1) * p.sk_np - 1) / p.sk_static);
 }
-
 // Partial slots of unit u (first cost unit us, end ue): static workers, then tail chunks,
 // overlapping it.
 __device__ __forceinline__ PartRanges unit_parts(const AttnParams& p, int u, int us, int ue) {
@@ -1144,6 +1174,23 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
   int blk = 0;   // block handoff sequence number (K-warp w and V-warp w+4 walk the same blocks)
   int nseg = 0;  // segment descriptor sequence number
 
+  if (p.fuse) {
+    // fused decode step, a4: worker P appends the new K (K-warp) / V (V-warp) token of units
+    // P, P + NP, ... and publishes it; readers wait on the flag (wait_ready) before the blocks
+    // the append touched (the evicted token's record, the window ring)
+    for (int a = (int)blockIdx.x * 4 + w; a < c.U; a += NP) {
+      append_unit_warp(c, is_k ? 0 : 1, a, (is_k ? p.k_new : p.v_new) + (size_t)a * kD, p.nc_old, p.nw_old, lane);
+      __syncwarp();
+      __threadfence();
+      if (lane == 0) {
+        if (is_k) {
+          if (p.evict) c.n_comp[a] = p.unc; else c.n_win[a] = p.unw;
+        }
+        publish_ready(p.ready + (is_k ? 0 : c.U) + a, p.epoch);
+      }
+    }
+  }
+
   if (is_k) {
     // ================= K-warp: schedule, scores + online softmax, P^T -> V-warp
     // Bookkeeping in shared memory, written by lane 0 (keeps it out of registers): [0] unit,
@@ -1154,7 +1201,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
     auto set_bounds = [&]() {  // lane 0: cost range of the segment -> item range [lo, hi)
       const int u0 = sg[0];
       const int us = unit_start(p, smem, u0), ue = unit_start(p, smem, u0 + 1);
-      const int nbc0 = (c.n_comp[u0] + 15) / 16;
+      const int nbc0 = (ncomp_of(p, u0) + 15) / 16;
       sg[3] = item_of_cost(p, sg[1] - us, nbc0, nwb);
       sg[4] = item_of_cost(p, min((int)sg[2], ue) - us, nbc0, nwb);
       sg[8] = ue;
@@ -1188,7 +1235,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
       __syncwarp();
       if (!sg[7]) break;
       const int u = sg[0];
-      const int n = c.n_comp[u];
+      const int n = ncomp_of(p, u);
       const int nbc = (n + 15) / 16;
       const int bbeg = min((int)sg[3], nbc), bend = min((int)sg[4], nbc);
       if (lane == 0 && (int)sg[4] > nbc) l2_prefetch(c.win[0] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
@@ -1238,6 +1285,8 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         // unit base pointers are re-derived per load (sg[0], params) to save registers
         auto load = [&](RawRegs<NK>& rr, int bb) {
           const size_t ub = (size_t)sg[0] * c.cap;
+          // the last block holds the record the fused append wrote: wait for its flag
+          if (p.fuse && p.evict && bb == nbc - 1) wait_ready(p.ready + u, p.epoch, lane);
           load_raw<NK>(rr, c.val[0] + ub * c.kpad[0], c.bm[0] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
         };
         RawRegs<NK> ra, rb;
@@ -1252,7 +1301,8 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
           ra = rb;  // waits for the prefetched block only after this block's work
         }
       }
-      const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
+      const int nw = nwin_of(p, u), first = c.W > 0 ? n % c.W : 0;
+      if (p.fuse && max((int)sg[3], nbc) < (int)sg[4]) wait_ready(p.ready + u, p.epoch, lane);
       for (int x = max((int)sg[3], nbc), hi = sg[4]; x < hi; ++x) {
         DenseBlock db;
         db.k = c.win[0] + (size_t)u * c.W * kD;
@@ -1270,7 +1320,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
             const uint4* pp = reinterpret_cast<const uint4*>(db.k + (size_t)(db.row0 + tok) * kD + 32 * t);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const uint4 a4 = pp[j];
+              const uint4 a4 = __ldcg(pp + j);
               kr[xx][4 * j] = a4.x; kr[xx][4 * j + 1] = a4.y; kr[xx][4 * j + 2] = a4.z; kr[xx][4 * j + 3] = a4.w;
             }
           } else {
@@ -1334,7 +1384,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         if (tracing && lane == 0) g_trace[kTraceW * cta + 8 + w] = global_ns();  // V-warp w done
         break;
       }
-      const int n = c.n_comp[u];
+      const int n = ncomp_of(p, u);
       const int nbc = (n + 15) / 16;
       const int bbeg = min(d.y, nbc), bend = min(d.z, nbc);
       if (lane == 0 && d.z > nbc) l2_prefetch(c.win[1] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
@@ -1382,6 +1432,8 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         // unit base pointers are re-derived per load (saves registers in the hot loop)
         auto load = [&](RawRegs<NV>& rr, int bb) {
           const size_t ub = (size_t)u * c.cap;
+          // the last block holds the record the fused append wrote: wait for its flag
+          if (p.fuse && p.evict && bb == nbc - 1) wait_ready(p.ready + c.U + u, p.epoch, lane);
           load_raw<NV>(rr, c.val[1] + ub * c.kpad[1], c.bm[1] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
         };
         RawRegs<NV> ra, rb;
@@ -1394,7 +1446,8 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
           ra = rb;
         }
       }
-      const int nw = c.n_win[u], first = c.W > 0 ? n % c.W : 0;
+      const int nw = nwin_of(p, u), first = c.W > 0 ? n % c.W : 0;
+      if (p.fuse && max(d.y, nbc) < d.z) wait_ready(p.ready + c.U + u, p.epoch, lane);
       for (int x = max(d.y, nbc); x < d.z; ++x) {
         DenseBlock db;
         db.k = c.win[0] + (size_t)u * c.W * kD;
@@ -1412,7 +1465,7 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
             const uint32_t* pp = reinterpret_cast<const uint32_t*>(db.v + (size_t)(db.row0 + tk[x4]) * kD) +
                                  16 * (g >> 1) + (g & 1);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) vr[x4][j] = pp[2 * j];
+            for (int j = 0; j < 8; ++j) vr[x4][j] = __ldcg(pp + 2 * j);
           } else {
 #pragma unroll
             for (int j = 0; j < 8; ++j) vr[x4][j] = 0;
@@ -1568,9 +1621,11 @@ int32_t max_splits_for(int32_t U, int32_t capacity) {
 }
 
 // Workspace header: [U] unit tickets (kv kernel) + [2] stream-K tail counters (zero between
-// calls), then the stream-K per-unit prefix [U+1].
+// calls), the stream-K per-unit prefix [U+1], the fused step's ready flags [2U].
+static size_t round256(size_t b) { return (b + 255) / 256 * 256; }
 static size_t ticket_bytes(int32_t U) {
-  return ((size_t)(U + 2) * sizeof(int) + 255) / 256 * 256 + ((size_t)(U + 1) * sizeof(int) + 255) / 256 * 256;
+  return round256((size_t)(U + 2) * sizeof(int)) + round256((size_t)(U + 1) * sizeof(int)) +
+         round256((size_t)2 * U * sizeof(int));
 }
 
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits) {
@@ -1688,7 +1743,9 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
 }
 
 cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, int32_t G, const uint16_t* q,
-                                    float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s) {
+                                    float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s,
+                                    const FuseArgs* fuse) {
+  if (fuse && !plan.sk) return cudaErrorInvalidValue;  // the fused step needs the register kernel
   AttnParams p;
   p.c = c;
   p.q = q;
@@ -1715,7 +1772,19 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.sk = 0;
   p.sk_static = p.sk_nb = p.sk_c = p.sk_nchunks = p.sk_total = 0;
   p.sk_ctr = p.tickets + c.U;
-  p.sk_pref = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ((size_t)(c.U + 2) * sizeof(int) + 255) / 256 * 256);
+  p.sk_pref = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + round256((size_t)(c.U + 2) * sizeof(int)));
+  p.ready = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + round256((size_t)(c.U + 2) * sizeof(int)) +
+                                   round256((size_t)(c.U + 1) * sizeof(int)));
+  p.fuse = fuse != nullptr;
+  p.k_new = fuse ? fuse->k_new : nullptr;
+  p.v_new = fuse ? fuse->v_new : nullptr;
+  p.nc_old = fuse ? fuse->nc_old : 0;
+  p.nw_old = fuse ? fuse->nw_old : 0;
+  p.unc = fuse ? fuse->unc : 0;
+  p.unw = fuse ? fuse->unw : 0;
+  p.evict = fuse ? fuse->evict : 0;
+  p.epoch = fuse ? fuse->epoch : 0;
+
   p.sk_np = 0;
   p.off_pref = 0;
   p.trace = std::getenv("MSTF_TRACE") != nullptr;  // dev timeline (tools/trace_ctas.py)

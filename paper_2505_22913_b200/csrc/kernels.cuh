@@ -84,8 +84,18 @@ void sk_cost_params(int32_t* cs, int32_t* cw);
 size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits);
 int32_t max_splits_for(int32_t U, int32_t capacity);
 
+// Fused decode step (append + attention in one register-kernel launch; uniform caches only).
+struct FuseArgs {
+  const uint16_t* k_new;
+  const uint16_t* v_new;
+  int32_t nc_old, nw_old;  // counters before the append (same for every unit)
+  int32_t unc, unw;        // after
+  int32_t evict;           // the oldest window token (or, W == 0, the new token) was compressed
+  int32_t epoch;           // stamp of this call's ready flags
+};
 cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, int32_t G, const uint16_t* q,
-                                    float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s);
+                                    float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s,
+                                    const FuseArgs* fuse = nullptr);
 
 cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const int32_t* lengths, int32_t U,
                                    int32_t G, int32_t t_max, int32_t splits, const uint16_t* q, float scale,

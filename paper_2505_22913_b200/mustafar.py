@@ -27,7 +27,8 @@ OUT_F32, OUT_F16 = 0, 1
 EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "mstf_cache_create",
            "mstf_cache_destroy", "mstf_cache_counts", "mstf_prune_compress_kv", "mstf_append_token",
            "mstf_workspace_bytes", "mstf_sparse_decode_attention", "mstf_dense_workspace_bytes",
-           "mstf_dense_decode_attention", "mstf_shard_units", "mstf_attention_kernel_count",
+           "mstf_dense_decode_attention", "mstf_shard_units", "mstf_decode_step",
+           "mstf_decode_step_kernel_count", "mstf_attention_kernel_count",
            "mstf_status_string", "mstf_build_info")
 
 
@@ -69,6 +70,8 @@ def lib() -> ctypes.CDLL:
         "mstf_dense_decode_attention": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, i32, vp, ctypes.c_float,
                                                        vp, i32, vp, sz, vp]),
         "mstf_shard_units": (ctypes.c_int, [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "mstf_decode_step": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_float, vp, i32, vp, sz, vp]),
+        "mstf_decode_step_kernel_count": (ctypes.c_int, [vp]),
         "mstf_attention_kernel_count": (ctypes.c_int, [vp]),
         "mstf_status_string": (ctypes.c_char_p, [i32]),
         "mstf_build_info": (ctypes.c_char_p, []),
@@ -221,6 +224,28 @@ class MustafarCache:
         """k_new, v_new: fp16 [U, d] (== [B, Hkv, d]) on the device."""
         _check("mstf_append_token", lib().mstf_append_token(self._h, _dev_ptr(k_new, name="k_new"),
                                                            _dev_ptr(v_new, name="v_new"), _stream(stream)))
+
+    def decode_step(self, k_new: torch.Tensor, v_new: torch.Tensor, q: torch.Tensor, scale=None, out=None,
+                    out_dtype=torch.float32, stream=None):
+        """append_token(k_new, v_new) then sparse_decode_attention(q) -- one fused launch when the
+        cache is uniform (mstf_decode_step). Returns out [U, G, d]."""
+        d = self.shape.head_dim
+        scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+        if out is None:
+            out = torch.empty((self.units, self.shape.group, d), dtype=out_dtype, device=self.device)
+        code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
+        _check("mstf_decode_step",
+               lib().mstf_decode_step(self._h, _dev_ptr(k_new, name="k_new"), _dev_ptr(v_new, name="v_new"),
+                                      _dev_ptr(q, name="q"), scale, _dev_ptr(out, out.dtype, "out"), code,
+                                      self._ws.data_ptr(), self._ws.numel(), _stream(stream)))
+        return out
+
+    def decode_step_kernel_count(self) -> int:
+        """Kernels one decode_step call launches in the cache's current state."""
+        n = lib().mstf_decode_step_kernel_count(self._h)
+        if n < 0:
+            _check("mstf_decode_step_kernel_count", n)
+        return n
 
     def sparse_decode_attention(self, q: torch.Tensor, scale=None, out=None, out_dtype=torch.float32,
                                 stream=None):

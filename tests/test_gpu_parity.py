@@ -235,3 +235,68 @@ def test_dense_baseline_matches_oracle(M, U, G, T):
     ref = np.stack([O.attention_dense(q[u].view(np.uint16), K[u, :lengths[u]].view(np.uint16),
                                       V[u, :lengths[u]].view(np.uint16), 1 / math.sqrt(128)) for u in range(U)])
     assert rel_err(out.cpu().numpy(), ref) <= TOL
+
+
+# --------------------------------------------------------------------------- fused decode step
+def _twin_caches(M, U_b, hq, hkv, T, kk, kv, W, steps, lengths=None, seed=11):
+    """Two GPU caches + one oracle cache with the same prefill, room for `steps` appends."""
+    U = U_b * hkv
+    K = synth.fp16_np((U, T + steps, 128), synth.seed_for(seed, 0))
+    V = synth.fp16_np((U, T + steps, 128), synth.seed_for(seed, 1))
+    cap = T + steps
+    Kd = torch.from_numpy(K.view(np.int16)).cuda().view(torch.float16)
+    Vd = torch.from_numpy(V.view(np.int16)).cuda().view(torch.float16)
+    caches = []
+    for _ in range(2):
+        c = M.MustafarCache(U_b, hq, hkv, 128, kk, kv, W, cap)
+        c.prune_compress_kv(Kd[:, :T].contiguous(), Vd[:, :T].contiguous(), lengths=lengths)
+        caches.append(c)
+    oc = O.OracleCache(U, 128, kk, kv, W, cap)
+    oc.prefill(K[:, :T].view(np.uint16), V[:, :T].view(np.uint16), lengths=lengths)
+    return caches, oc, K, V, Kd, Vd
+
+
+@pytest.mark.parametrize("case", [
+    # (batch, hq, hkv, T, keep_k, keep_v, W, steps, lengths)
+    (16, 32, 8, 600, 39, 39, 32, 5, None),      # full window: every step evicts into a record
+    (2, 8, 2, 10, 39, 39, 32, 30, None),        # window filling (no eviction), then evicting
+    (2, 8, 2, 300, 39, 39, 0, 4, None),         # W = 0: the new token is compressed directly
+    (1, 8, 1, 777, 32, 32, 32, 3, None),        # G = 8, k_pad 32
+    (2, 8, 2, 400, 39, 39, 32, 3, [400, 37, 1, 64]),  # ragged: append + attention in sequence
+    (1, 8, 2, 300, 64, 64, 32, 3, None),        # k_pad 64 (TMA kernel): unfused
+    (200, 16, 8, 40, 39, 39, 32, 2, None),      # 1600 units > 1184 workers (appends loop)
+])
+def test_decode_step_equals_append_then_attention(M, case):
+    U_b, hq, hkv, T, kk, kv, W, steps, lengths = case
+    U, G = U_b * hkv, hq // hkv
+    (cf, cs), oc, K, V, Kd, Vd = _twin_caches(M, U_b, hq, hkv, T, kk, kv, W, steps, lengths)
+    scale = 1 / math.sqrt(128)
+    for i in range(steps):
+        q = synth.fp16_np((U, G, 128), synth.seed_for(500 + i, 2))
+        qd = torch.from_numpy(q.view(np.int16)).cuda().view(torch.float16)
+        kn, vn = Kd[:, T + i].contiguous(), Vd[:, T + i].contiguous()
+        fused = lengths is None and kk == kv and kk != 64
+        assert cf.decode_step_kernel_count() == (2 if fused else 3)
+        of = cf.decode_step(kn, vn, qd, scale)
+        cs.append_token(kn, vn)
+        os_ = cs.sparse_decode_attention(qd, scale)
+        oc.append(K[:, T + i].view(np.uint16), V[:, T + i].view(np.uint16))
+        torch.cuda.synchronize()
+        # same plan, same arithmetic: the fused launch reproduces the two-call result exactly
+        assert torch.equal(of, os_), (case, i, (of - os_).abs().max().item())
+        assert rel_err(of.cpu().numpy(), O.attention(oc, q.view(np.uint16), scale)) <= TOL
+    compare_cache(cf, oc, "fused")
+    assert cf.counts() == cs.counts()
+
+
+def test_decode_step_capacity_error(M):
+    """A step that would compress past `capacity` is rejected before any launch, like append."""
+    T, W = 40, 32
+    K = torch.zeros(1, T, 128, dtype=torch.float16, device="cuda")
+    c = M.MustafarCache(1, 4, 1, 128, 39, 39, W, T - W)  # compressed capacity exactly used by the prefill
+    c.prune_compress_kv(K, K)
+    q = torch.zeros(1, 4, 128, dtype=torch.float16, device="cuda")
+    kn = torch.zeros(1, 128, dtype=torch.float16, device="cuda")
+    with pytest.raises(M.MustafarError):
+        c.decode_step(kn, kn, q)
+    assert c.counts() == ([T - W], [W])
