@@ -195,6 +195,13 @@ int check_attention_args(const mstf_cache* h, const void* q, const void* out, in
   return MSTF_OK;
 }
 
+// Every unit has the same counters (the fused decode step's precondition).
+bool uniform_counters(const mstf_cache* h) {
+  for (int32_t u = 1; u < h->view.U; ++u)
+    if (h->nc[u] != h->nc[0] || h->nw[u] != h->nw[0]) return false;
+  return true;
+}
+
 // Stamp of a fused step's ready flags: unique across calls and caches of the process.
 int32_t next_epoch() {
   static std::atomic<int32_t> e{0};
@@ -230,10 +237,9 @@ int mstf_decode_step(mstf_cache* h, const void* k_new, const void* v_new, const 
   for (int32_t u = 0; u < U; ++u)
     if ((W == 0 || h->nw[u] == W) && h->nc[u] + 1 > h->view.cap) return MSTF_ECAPACITY;
   // counters after the append (a4)
+  const bool uniform = uniform_counters(h);
   std::vector<int32_t> nc = h->nc, nw = h->nw;
-  bool uniform = true;
   for (int32_t u = 0; u < U; ++u) {
-    uniform = uniform && nc[u] == nc[0] && nw[u] == nw[0];
     if (W == 0 || nw[u] == W) nc[u] += 1; else nw[u] += 1;
   }
   AttnPlan plan;
@@ -264,10 +270,15 @@ int mstf_decode_step(mstf_cache* h, const void* k_new, const void* v_new, const 
 
 int mstf_decode_step_kernel_count(const mstf_cache* h) {
   if (!h) return MSTF_EINVAL;
-  bool uniform = true;
-  for (int32_t u = 1; u < h->view.U; ++u) uniform = uniform && h->nc[u] == h->nc[0] && h->nw[u] == h->nw[0];
-  // fused (register kernel + combine) or append + attention + combine
-  return uniform && uses_reg_kernel(h->view.kpad[0], h->view.kpad[1]) ? 2 : 3;
+  // mirrors mstf_decode_step: fused (register kernel + combine) or append + attention + combine
+  const int32_t U = h->view.U, W = h->view.W;
+  std::vector<int32_t> nc = h->nc, nw = h->nw;
+  for (int32_t u = 0; u < U; ++u) {
+    if (W == 0 || nw[u] == W) nc[u] += 1; else nw[u] += 1;
+  }
+  AttnPlan plan;
+  if (make_plan(h, nc, nw, &plan) != MSTF_OK) return 3;
+  return uniform_counters(h) && plan.sk ? 2 : 3;
 }
 
 static int32_t dense_splits(int32_t units, int32_t t_max) {
