@@ -253,28 +253,47 @@ def run_ours(args, cfg, rank, world, local_rank):
     nc, nw = caches[0].counts()
     n_comp, n_win = nc[0], nw[0]
 
-    # ---- end to end through the public API with host buffers (pinned), copies inside the timing
-    host_in = torch.empty((K_steps, L, per_layer), dtype=torch.float16, pin_memory=True)
-    host_in.copy_(gen[W_steps:W_steps + K_steps].cpu())  # same inputs as the headline pass
-    host_out = torch.empty((U, G, d), dtype=torch.float16, pin_memory=True)
-    dev_in = torch.empty((L, per_layer), dtype=torch.float16, device=dev)
-    # re-run the same steps on fresh caches would change n_comp; use the live caches (state moves on)
+    # ---- end to end through the public API with host buffers (pinned), copies inside the timing.
+    # Every step copies its inputs (q, k_new, v_new of all layers) host -> device and reads its
+    # result (the last layer's output) back to the host. The copy of step s+1 runs on a copy
+    # stream while step s computes (double-buffered device inputs); one sync at the end.
+    e2e_steps = min(K_steps, cap - (n_comp + 1))  # the caches' remaining headroom
+    e2e_steps = max(1, min(e2e_steps, 8))
+    host_in = torch.empty((e2e_steps, L, per_layer), dtype=torch.float16, pin_memory=True)
+    host_in.copy_(gen[W_steps:W_steps + e2e_steps].cpu())  # same inputs as the headline pass
+    host_out = torch.empty((e2e_steps, U, G, d), dtype=torch.float16, pin_memory=True)
+    dev_in = [torch.empty((L, per_layer), dtype=torch.float16, device=dev) for _ in range(2)]
+    copy_stream = torch.cuda.Stream(device=dev)
+    compute = torch.cuda.current_stream()
+    ready = [torch.cuda.Event() for _ in range(2)]      # inputs of buffer b are on the device
+    consumed = [torch.cuda.Event() for _ in range(2)]   # the step reading buffer b has run
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # the caches have capacity for total_steps appends; e2e re-uses the remaining headroom
-    e2e_steps = min(K_steps, cap - (n_comp + 1))
-    e2e_steps = max(1, min(e2e_steps, 8))
-    f0.record()
+
+    def h2d(s_, b_):
+        with torch.cuda.stream(copy_stream):
+            dev_in[b_].copy_(host_in[s_], non_blocking=True)
+            ready[b_].record(copy_stream)
+
+    f0.record(compute)
+    copy_stream.wait_stream(compute)  # the first copy starts inside the timed region
+    h2d(0, 0)
     for s in range(e2e_steps):
-        dev_in.copy_(host_in[s], non_blocking=True)
-        step(dev_in)
-        host_out.copy_(outs[L - 1], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-    f1.record()
+        b = s % 2
+        if s + 1 < e2e_steps:
+            if s >= 1:
+                copy_stream.wait_event(consumed[1 - b])  # step s-1 has read that buffer
+            h2d(s + 1, 1 - b)
+        compute.wait_event(ready[b])
+        step(dev_in[b])
+        consumed[b].record(compute)
+        host_out[s].copy_(outs[L - 1], non_blocking=True)
+    f1.record(compute)
     torch.cuda.synchronize()
     e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    assert torch.isfinite(host_out.float()).all()
 
     # ---- dense-KV baselines (same shapes, dense fp16 KV of all L layers)
     dense = {}
