@@ -1058,12 +1058,17 @@ __device__ __forceinline__ int ncomp_of(const AttnParams& p, int u) { return p.f
 __device__ __forceinline__ int nwin_of(const AttnParams& p, int u) { return p.fuse ? p.unw : p.c.n_win[u]; }
 
 // Fused step: wait until the warp that appended this unit's tensor published it.
+// The appending warp runs at the start of a lower-indexed CTA, so the wait is short; a bounded
+// spin (~1 s) turns a broken invariant into a launch error (trap) instead of a hung GPU.
 __device__ __forceinline__ void wait_ready(const int* flag, int epoch, int lane) {
   if (lane == 0) {
     int v;
-    do {
+    for (uint32_t it = 0;; ++it) {
       asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    } while (v != epoch);
+      if (v == epoch) break;
+      if (it > (1u << 22)) __trap();
+      __nanosleep(64);
+    }
   }
   __syncwarp();
 }
