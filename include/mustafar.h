@@ -80,7 +80,10 @@ int32_t mstf_k_pad(int32_t keep);
  *   BITMAP_x  u64 [U][capacity][d/64]  bit i of word j <=> channel 64j+i kept (LSB first);
  *                                       exactly keep_x bits set per record (R4)
  *   VALUES_x  u16 [U][capacity][kpad]   kept fp16 bit patterns in ascending channel order,
- *                                       then 0x0000 up to kpad = mstf_k_pad(keep_x) (R6, R7)
+ *                                       then 0x0000 up to kpad = mstf_k_pad(keep_x) (R6, R7);
+ *                                       the buffer is 16 bytes longer (tail guard: the
+ *                                       attention kernels read, never use, up to 8 bytes
+ *                                       past the last record)
  *   OFFSETS_x u32 [U][capacity][d/64]   p*kpad + (kept channels in tiles < j): element index
  *                                       of tile j's first value in the unit's value array (R8)
  *   WIN_x     u16 [U][max(W,1)][d]      dense window ring: token p sits in slot p % W (R9)

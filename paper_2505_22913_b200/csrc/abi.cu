@@ -63,8 +63,9 @@ int mstf_cache_buffer_bytes(const mstf_config* c, size_t sizes[MSTF_NUM_BUFFERS]
   const size_t U = (size_t)c->batch * c->num_kv_heads, cap = c->capacity, nt = c->head_dim / 64;
   const size_t W = c->window > 0 ? c->window : 1;
   sizes[MSTF_BUF_BITMAP_K] = sizes[MSTF_BUF_BITMAP_V] = U * cap * nt * 8;
-  sizes[MSTF_BUF_VALUES_K] = U * cap * mstf_k_pad(c->keep_k) * 2;
-  sizes[MSTF_BUF_VALUES_V] = U * cap * mstf_k_pad(c->keep_v) * 2;
+  // + kValuesGuard: the attention kernels' per-token loads may read up to 8 bytes past a record
+  sizes[MSTF_BUF_VALUES_K] = U * cap * mstf_k_pad(c->keep_k) * 2 + kValuesGuard;
+  sizes[MSTF_BUF_VALUES_V] = U * cap * mstf_k_pad(c->keep_v) * 2 + kValuesGuard;
   sizes[MSTF_BUF_OFFSETS_K] = sizes[MSTF_BUF_OFFSETS_V] = U * cap * nt * 4;
   sizes[MSTF_BUF_WIN_K] = sizes[MSTF_BUF_WIN_V] = U * W * c->head_dim * 2;
   sizes[MSTF_BUF_N_COMP] = sizes[MSTF_BUF_N_WIN] = U * 4;

@@ -965,10 +965,11 @@ __device__ __forceinline__ void load_raw(RawRegs<NCH>& rr, const uint16_t* __res
   const bool ok = tau < nvalid;
   auto ld = [](const uint32_t* a) { return __ldca(a); };
   rr.W[0] = (h && ok) ? ld(src) : 0u;
-  // the upper half's last words lie past the token (they only feed pair entries beyond k_pad,
-  // which no gather reads): zero instead of loading, so the last record is never overrun
+  // the upper half's last two words lie past the token (they only feed pair entries beyond
+  // k_pad, which no gather reads); the values buffers carry a 16-byte tail guard
+  // (mstf_cache_buffer_bytes) so the last record's overrun stays inside the allocation
 #pragma unroll
-  for (int i = 1; i < Gm::nw; ++i) rr.W[i] = (ok && (h == 0 || i < Gm::kp / 4)) ? ld(src + i) : 0u;
+  for (int i = 1; i < Gm::nw; ++i) rr.W[i] = ok ? ld(src + i) : 0u;
   const uint32_t* bw = reinterpret_cast<const uint32_t*>(bms);
   rr.bm0 = g < nvalid ? ld(bw + (size_t)(tok0 + g) * 4 + t) : 0u;
   rr.bm1 = g + 8 < nvalid ? ld(bw + (size_t)(tok0 + g + 8) * 4 + t) : 0u;

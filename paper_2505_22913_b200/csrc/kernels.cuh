@@ -36,6 +36,7 @@ constexpr int kTiles = kD / 64;  // 64-bit bitmap words per token record
 constexpr int kChunk = 64;       // tokens per TMA stage
 constexpr int kConsumerWarps = 4;
 constexpr int kMaxGroup = 8;     // query heads per unit (mma N = 8)
+constexpr int kValuesGuard = 16; // bytes after each VALUES buffer (read past the last record, never used)
 constexpr int kMaxSkGrid = 2 * 148;  // stream-K grid cap (2 CTAs per SM on a B200)
 constexpr int kMaxSkPrefix = 16384;  // ragged stream-K: max units (prefix array in smem)
 constexpr int kSkChunksPerWorker = 2;  // stream-K dynamic tail: at most this many chunks per warp pair

@@ -187,8 +187,9 @@ class MustafarCache:
         return {
             "bitmap_k": r["bitmap_k"].view(torch.int64).view(U, cap, nt),
             "bitmap_v": r["bitmap_v"].view(torch.int64).view(U, cap, nt),
-            "values_k": r["values_k"].view(torch.int16).view(U, cap, k_pad(self.keep_k)),
-            "values_v": r["values_v"].view(torch.int16).view(U, cap, k_pad(self.keep_v)),
+            # the values buffers end with a 16-byte tail guard (include/mustafar.h)
+            "values_k": r["values_k"][:U * cap * k_pad(self.keep_k) * 2].view(torch.int16).view(U, cap, k_pad(self.keep_k)),
+            "values_v": r["values_v"][:U * cap * k_pad(self.keep_v) * 2].view(torch.int16).view(U, cap, k_pad(self.keep_v)),
             "offsets_k": r["offsets_k"].view(torch.int32).view(U, cap, nt),
             "offsets_v": r["offsets_v"].view(torch.int32).view(U, cap, nt),
             "win_k": r["win_k"].view(torch.int16).view(U, W, d),

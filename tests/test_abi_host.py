@@ -57,8 +57,9 @@ def cfg(**kw):
 def test_buffer_bytes(L):
     sizes = M.buffer_bytes(cfg())
     U = 4
-    assert sizes == [U * 100 * 16, U * 100 * 16, U * 100 * 40 * 2, U * 100 * 64 * 2, U * 100 * 8, U * 100 * 8,
-                     U * 32 * 128 * 2, U * 32 * 128 * 2, U * 4, U * 4]
+    guard = 16  # values buffers: tail guard for the attention kernels' per-token loads
+    assert sizes == [U * 100 * 16, U * 100 * 16, U * 100 * 40 * 2 + guard, U * 100 * 64 * 2 + guard,
+                     U * 100 * 8, U * 100 * 8, U * 32 * 128 * 2, U * 32 * 128 * 2, U * 4, U * 4]
 
 
 @pytest.mark.parametrize("kw,code", [
