@@ -66,3 +66,34 @@ def test_fullsize_sampled(M, name):
         o = out[u].cpu().numpy().astype(np.float64)
         err = float((np.abs(o - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max())
         assert err <= TOL, (name, u, err)
+
+
+@pytest.mark.parametrize("name", ["C2_b16_s70", "C4_128k_b8"])
+def test_fullsize_decode_step_sampled(M, name):
+    """One fused decode step (mstf_decode_step: the append inside the attention launch) at full
+    size, against the oracle on sampled units."""
+    B, hq, hkv, T, sk, sv, sample = CASES[name]
+    U, G, d, W = B * hkv, hq // hkv, 128, 32
+    kk, kv = O.keep_count(sk, d), O.keep_count(sv, d)
+    sK, sV, sQ = (synth.seed_for(8, i) for i in range(3))
+    K = synth.fp16_torch((U, T + 1, d), sK, device="cuda")
+    V = synth.fp16_torch((U, T + 1, d), sV, device="cuda")
+    q = synth.fp16_torch((U, G, d), sQ, device="cuda")
+    gc = M.MustafarCache(B, hq, hkv, d, kk, kv, W, T + 1)
+    gc.prune_compress_kv(K[:, :T].contiguous(), V[:, :T].contiguous())
+    kn, vn = K[:, T].contiguous(), V[:, T].contiguous()
+    del K, V
+    assert gc.decode_step_kernel_count() == 2
+    out = gc.decode_step(kn, vn, q, 1 / math.sqrt(d))
+    torch.cuda.synchronize()
+    qh = q.cpu().view(torch.int16).numpy().view(np.uint16)
+    for u in sample:
+        Ku = synth.fp16_np_rows((U, T + 1, d), sK, u * (T + 1), T + 1).view(np.uint16)
+        Vu = synth.fp16_np_rows((U, T + 1, d), sV, u * (T + 1), T + 1).view(np.uint16)
+        oc = O.OracleCache(1, d, kk, kv, W, T + 1)
+        oc.prefill(Ku[None, :T], Vu[None, :T])
+        oc.append(Ku[None, T], Vu[None, T])
+        ref = O.attention(oc, qh[u][None], 1 / math.sqrt(d))[0]
+        o = out[u].cpu().numpy().astype(np.float64)
+        err = float((np.abs(o - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max())
+        assert err <= TOL, (name, u, err)
