@@ -17,13 +17,13 @@
 // (prmt sign-replicate masks), so a lane builds its fragments without branches.
 //
 // Kernels
-//   mstf_attn_reg_kernel<NK,NV>   (kpad 16/32/40; the 70%-sparsity path) 8 warps, each
+//   mstf_attn_reg_kernel<NK,NV>   (k_pad 16/32/40/64: the 70% and 50% sparsity paths) 8 warps, each
 //       warp streams its blocks' records straight into registers with a one-block
 //       software pipeline, builds the pair arrays from registers, gathers, mma. Work
 //       schedule: stream-K (units' blocks concatenated, equal ranges over one wave of
 //       2 CTAs per SM; see UnitSched below) or split grid (S, U). The last CTA to finish
 //       a unit merges its partials (a9) in the same launch.
-//   mstf_attn_kv_kernel<NK,NV,I>  (other kpad, e.g. 64 at 50% sparsity) 8 consumer warps +
+//   mstf_attn_kv_kernel<NK,NV,I>  (other k_pad, or K != V sparsity) 8 consumer warps +
 //       1 producer warp streaming 64-token chunks (K bitmaps, K values, V bitmaps,
 //       V values: four cp.async.bulk copies) into an mbarrier-guarded smem ring; split grid.
 //   mstf_combine_kernel           merges the kv kernel's split partials (a9).
@@ -961,15 +961,33 @@ __device__ __forceinline__ void load_raw(RawRegs<NCH>& rr, const uint16_t* __res
   const int tau = lane >> 1, h = lane & 1, g = lane >> 2, t = lane & 3;
   const int m0 = h ? Gm::kp / 2 + 2 : 0;
   // words wb .. wb + nw - 1 of token tok0 + tau, wb = m0/2 - 1 (h = 0: word -1 is zero)
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(vals + (size_t)(tok0 + tau) * Gm::kp) + (m0 / 2 - 1);
   const bool ok = tau < nvalid;
   auto ld = [](const uint32_t* a) { return __ldca(a); };
+  if constexpr (NCH >= 8) {
+  // k_pad >= 64: both halves load nw words from an 8-byte aligned start (word 0 / word kp/4)
+  // with 64-bit loads, then the lower half shifts by one word (its W[0] is the zero word -1).
+  // Half the load instructions and L1 sector lookups of the scalar path (the L1 data pipe is
+  // the bound at 50% density); at k_pad 40 the extra selects cost more than they save.
+  const uint2* vsrc = reinterpret_cast<const uint2*>(vals + (size_t)(tok0 + tau) * Gm::kp + (h ? Gm::kp / 2 : 0));
+  uint32_t T[Gm::nw + 1];
+#pragma unroll
+  for (int i = 0; i < (Gm::nw + 1) / 2; ++i) {
+    const uint2 x = ok ? __ldca(vsrc + i) : make_uint2(0u, 0u);
+    T[2 * i] = x.x;
+    if (2 * i + 1 < Gm::nw + 1) T[2 * i + 1] = x.y;
+  }
+  rr.W[0] = h ? T[0] : 0u;
+#pragma unroll
+  for (int i = 1; i < Gm::nw; ++i) rr.W[i] = h ? T[i] : T[i - 1];
+  } else {
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(vals + (size_t)(tok0 + tau) * Gm::kp) + (m0 / 2 - 1);
   rr.W[0] = (h && ok) ? ld(src) : 0u;
   // the upper half's last two words lie past the token (they only feed pair entries beyond
   // k_pad, which no gather reads); the values buffers carry a 16-byte tail guard
   // (mstf_cache_buffer_bytes) so the last record's overrun stays inside the allocation
 #pragma unroll
   for (int i = 1; i < Gm::nw; ++i) rr.W[i] = ok ? ld(src + i) : 0u;
+  }
   const uint32_t* bw = reinterpret_cast<const uint32_t*>(bms);
   rr.bm0 = g < nvalid ? ld(bw + (size_t)(tok0 + g) * 4 + t) : 0u;
   rr.bm1 = g + 8 < nvalid ? ld(bw + (size_t)(tok0 + g + 8) * 4 + t) : 0u;
@@ -1680,11 +1698,11 @@ int32_t sk_unit_cost(int32_t n_comp, int32_t W) {
   return cs + (n_comp + 15) / 16 + (W > 0 ? (W + 15) / 16 : 0) * cw;
 }
 
-// Register-staged kernel (stream-K + combine kernel) for equal K/V k_pad of 16, 32 or 40;
+// Register-staged kernel (stream-K + combine kernel) for equal K/V k_pad of 16, 32, 40 or 64;
 // the TMA-staged kernel + separate combine otherwise.
 bool uses_reg_kernel(int32_t kpad_k, int32_t kpad_v) {
   const int32_t nk = kpad_k / 8;
-  return kpad_k == kpad_v && (nk == 2 || nk == 4 || nk == 5);
+  return kpad_k == kpad_v && (nk == 2 || nk == 4 || nk == 5 || nk == 8);
 }
 
 AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_t uniform_items,
@@ -1815,6 +1833,7 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
     switch (nk) {
       case 2: rk = mstf_attn_reg_kernel<2, 2>; break;
       case 4: rk = mstf_attn_reg_kernel<4, 4>; break;
+      case 8: rk = mstf_attn_reg_kernel<8, 8>; break;
       default: rk = mstf_attn_reg_kernel<5, 5>; break;
     }
     AttnParams pr = p;

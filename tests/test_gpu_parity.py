@@ -177,6 +177,7 @@ def test_attention_ragged_units(M):
     (64, 8, 2, 300, 39, 32, [(37 * i) % 300 + 1 for i in range(128)]),  # ragged, many units
     (2, 8, 2, 1000, 32, 32, [1000, 17, 16, 999]),                     # kpad 32 kernel
     (2, 8, 2, 1000, 16, 16, None),                                    # kpad 16 kernel
+    (4, 16, 4, 700, 64, 64, [700, 5, 64, 333] * 4),                   # kpad 64 (50% sparsity)
 ])
 def test_attention_schedules(M, monkeypatch, sched, case):
     """Both work schedules of the register-staged kernel (split grid; stream-K with units
@@ -263,7 +264,8 @@ def _twin_caches(M, U_b, hq, hkv, T, kk, kv, W, steps, lengths=None, seed=11):
     (2, 8, 2, 300, 39, 39, 0, 4, None),         # W = 0: the new token is compressed directly
     (1, 8, 1, 777, 32, 32, 32, 3, None),        # G = 8, k_pad 32
     (2, 8, 2, 400, 39, 39, 32, 3, [400, 37, 1, 64]),  # ragged: append + attention in sequence
-    (1, 8, 2, 300, 64, 64, 32, 3, None),        # k_pad 64 (TMA kernel): unfused
+    (1, 8, 2, 300, 64, 64, 32, 3, None),        # k_pad 64 (register kernel, vector loads): fused
+    (1, 8, 2, 300, 26, 39, 32, 3, None),        # K != V sparsity (TMA kernel): unfused
     (200, 16, 8, 40, 39, 39, 32, 2, None),      # 1600 units > 1184 workers (appends loop)
 ])
 def test_decode_step_equals_append_then_attention(M, case):
@@ -275,7 +277,7 @@ def test_decode_step_equals_append_then_attention(M, case):
         q = synth.fp16_np((U, G, 128), synth.seed_for(500 + i, 2))
         qd = torch.from_numpy(q.view(np.int16)).cuda().view(torch.float16)
         kn, vn = Kd[:, T + i].contiguous(), Vd[:, T + i].contiguous()
-        fused = lengths is None and kk == kv and kk != 64
+        fused = lengths is None and kk == kv and O.k_pad_of(kk) in (16, 32, 40, 64)
         assert cf.decode_step_kernel_count() == (2 if fused else 3)
         of = cf.decode_step(kn, vn, qd, scale)
         cs.append_token(kn, vn)
