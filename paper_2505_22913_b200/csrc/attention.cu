@@ -1289,24 +1289,6 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         if (lane == 0) mbar_arrive(&hfull[2 * w + hs]);
         ++blk;
       };
-      auto k_step = [&](const RawRegs<NK>& cur, int b) {
-        const int nvalid = min(16, n - b * 16);
-        __syncwarp();
-        store_pairs<NK, false>(smem, cur, ybase, lane);
-        const uint32_t pk = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
-        uint32_t ik = pk;
-#pragma unroll
-        for (int o = 1; o < 4; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
-          if (t >= o) ik += y;
-        }
-        const uint32_t ek = ik - pk;
-        __syncwarp();
-        uint32_t kr[2][16];
-        gather16_s<32>(smem, cur.bm0, ybase + 4u * (uint32_t)(KLayout<NK>::k0 + g) + 32u * (ek & 0xFFFF), kr[0]);
-        gather16_s<32>(smem, cur.bm1, ybase + 4u * (uint32_t)(KLayout<NK>::k1 + g) + 32u * (ek >> 16), kr[1]);
-        handoff_put(k_block(kr, g < nvalid, g + 8 < nvalid, st, p.scale_log2));
-      };
       {
         // unit base pointers are re-derived per load (sg[0], params) to save registers
         auto load = [&](RawRegs<NK>& rr, int bb) {
@@ -1315,16 +1297,33 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
           if (p.fuse && p.evict && bb == nbc - 1) wait_ready(p.ready + u, p.epoch, lane);
           load_raw<NK>(rr, c.val[0] + ub * c.kpad[0], c.bm[0] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
         };
-        RawRegs<NK> ra, rb;
-        int b = bbeg;
-        if (b < bend) load(ra, b);
         // One loop body (not a two-way unrolled ping-pong): the kernel's code footprint is what
-        // the instruction cache sees with K- and V-warps resident together (-10% time, measured).
+        // the instruction cache sees with K- and V-warps resident together. One raw buffer:
+        // once a block's words are in the pair array its registers are dead, so the next
+        // block's loads go into them right away and overlap the gathers, MMAs and softmax.
+        RawRegs<NK> rr;
+        int b = bbeg;
+        if (b < bend) load(rr, b);
 #pragma unroll 1
         for (; b < bend; ++b) {
-          if (b + 1 < bend) load(rb, b + 1);
-          k_step(ra, b);
-          ra = rb;  // waits for the prefetched block only after this block's work
+          const int nvalid = min(16, n - b * 16);
+          __syncwarp();
+          store_pairs<NK, false>(smem, rr, ybase, lane);
+          const uint32_t bm0 = rr.bm0, bm1 = rr.bm1;
+          if (b + 1 < bend) load(rr, b + 1);
+          const uint32_t pk = __popc(bm0) | (__popc(bm1) << 16);
+          uint32_t ik = pk;
+#pragma unroll
+          for (int o = 1; o < 4; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
+            if (t >= o) ik += y;
+          }
+          const uint32_t ek = ik - pk;
+          __syncwarp();
+          uint32_t kr[2][16];
+          gather16_s<32>(smem, bm0, ybase + 4u * (uint32_t)(KLayout<NK>::k0 + g) + 32u * (ek & 0xFFFF), kr[0]);
+          gather16_s<32>(smem, bm1, ybase + 4u * (uint32_t)(KLayout<NK>::k1 + g) + 32u * (ek >> 16), kr[1]);
+          handoff_put(k_block(kr, g < nvalid, g + 8 < nvalid, st, p.scale_log2));
         }
       }
       const int nw = nwin_of(p, u), first = c.W > 0 ? n % c.W : 0;
@@ -1428,32 +1427,6 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         ++blk;
         return hh;
       };
-      auto v_step = [&](const RawRegs<NV>& cur) {
-        __syncwarp();
-        store_pairs<NV, true>(smem, cur, ybase, lane);
-        const uint32_t pv = __popc(cur.bm0) | (__popc(cur.bm1) << 16);
-        uint32_t iv = pv;
-#pragma unroll
-        for (int o = 1; o < 4; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o, 4);
-          if (t >= o) iv += y;
-        }
-        const uint32_t ev = iv - pv;
-        __syncwarp();
-        const int sa = 8 * t + (g >> 1), sb = sa + 4;
-        const uint32_t w2t = __shfl_sync(0xffffffffu, cur.bm0, sa), w2t8 = __shfl_sync(0xffffffffu, cur.bm1, sa);
-        const uint32_t w2t1 = __shfl_sync(0xffffffffu, cur.bm0, sb), w2t9 = __shfl_sync(0xffffffffu, cur.bm1, sb);
-        const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
-        const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
-        const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
-        uint32_t vr[4][8];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const uint32_t base = smem_u32(smem) + ybase + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * ps[x];
-          gather8_il<16>(ws[x], opaque(base), g & 1, vr[x]);
-        }
-        v_block(vr, handoff_get(), acc);
-      };
       {
         // unit base pointers are re-derived per load (saves registers in the hot loop)
         auto load = [&](RawRegs<NV>& rr, int bb) {
@@ -1462,14 +1435,38 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
           if (p.fuse && p.evict && bb == nbc - 1) wait_ready(p.ready + c.U + u, p.epoch, lane);
           load_raw<NV>(rr, c.val[1] + ub * c.kpad[1], c.bm[1] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
         };
-        RawRegs<NV> ra, rb;
+        // one raw buffer: refilled with the next block as soon as this block's pair array and
+        // bitmap words are extracted (see the K-warp loop)
+        RawRegs<NV> rr;
         int b = bbeg;
-        if (b < bend) load(ra, b);
+        if (b < bend) load(rr, b);
 #pragma unroll 1
         for (; b < bend; ++b) {
-          if (b + 1 < bend) load(rb, b + 1);
-          v_step(ra);
-          ra = rb;
+          __syncwarp();
+          store_pairs<NV, true>(smem, rr, ybase, lane);
+          const uint32_t pv = __popc(rr.bm0) | (__popc(rr.bm1) << 16);
+          uint32_t iv = pv;
+#pragma unroll
+          for (int o = 1; o < 4; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, iv, o, 4);
+            if (t >= o) iv += y;
+          }
+          const uint32_t ev = iv - pv;
+          const int sa = 8 * t + (g >> 1), sb = sa + 4;
+          const uint32_t w2t = __shfl_sync(0xffffffffu, rr.bm0, sa), w2t8 = __shfl_sync(0xffffffffu, rr.bm1, sa);
+          const uint32_t w2t1 = __shfl_sync(0xffffffffu, rr.bm0, sb), w2t9 = __shfl_sync(0xffffffffu, rr.bm1, sb);
+          const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
+          if (b + 1 < bend) load(rr, b + 1);
+          __syncwarp();
+          const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
+          const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
+          uint32_t vr[4][8];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const uint32_t base = smem_u32(smem) + ybase + 4u * (uint32_t)(VLayout<NV>::region(x) + t) + 16u * ps[x];
+            gather8_il<16>(ws[x], opaque(base), g & 1, vr[x]);
+          }
+          v_block(vr, handoff_get(), acc);
         }
       }
       const int nw = nwin_of(p, u), first = c.W > 0 ? n % c.W : 0;
@@ -1740,6 +1737,7 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
   if (uses_reg_kernel(kpad_k, kpad_v) && total_items > 0 && total_items < (1ll << 30) &&
       (uniform_items > 0 || U <= kMaxSkPrefix)) {
     int64_t grid = 2 * (int64_t)sm_count;
+    if (const char* e = std::getenv("MSTF_SKGRID")) grid = std::atoi(e);  // dev: occupancy scan
     if (grid > kMaxSkGrid) grid = kMaxSkGrid;
     const int64_t min_q = 8;  // >= 2 items per worker to amortise the segment prologue
     if (grid > (total_items + min_q - 1) / min_q) grid = (total_items + min_q - 1) / min_q;
