@@ -1,14 +1,18 @@
 // compress.cu -- K1: runtime per-token magnitude pruning + bitmap compression.
 //
-// One warp per token vector (d = 128, lane l owns channels 4l..4l+3, one 8-byte load).
 //   a1  magnitude key  mag_c = bits_c & 0x7FFF (R3: fp16 magnitude as an unsigned integer)
-//   a2  top-k select   tau = the k-th largest magnitude, found by a 15-step bisection on the
-//                      magnitude bits with one redux.sync per step; channels with
-//                      mag > tau are kept, and among mag == tau the (k - #{mag > tau})
-//                      HIGHEST channel indices (ties prune the lower index first, R2)
-//   a3  bitmap + pack  4 redux.or build the 128-bit keep mask (bit c <-> channel c, R6),
-//                      popcount prefix sums give each kept value its packed slot, padding
-//                      slots [k, kpad) are 0x0000 (R7), tile offsets p*kpad + popc(tiles<j) (R8)
+//   a2  top-k select   tau = the k-th largest magnitude, found MSB-first (15 steps) with SWAR
+//                      compares and one warp sum per step; channels with mag > tau are kept,
+//                      and among mag == tau the (k - #{mag > tau}) HIGHEST channel indices
+//                      (ties prune the lower index first, R2)
+//   a3  bitmap + pack  bit c <-> channel c (R6); popcount prefix sums give each kept value its
+//                      packed slot, padding slots [k, kpad) are 0x0000 (R7), tile offsets
+//                      p*kpad + popc(tiles<j) (R8)
+// Two layouts of the same computation:
+//   bulk (prefill_kernel)   four tokens per warp, eight lanes x 16 channels per token; one warp
+//                           sum carries the four tokens' counts in separate bytes
+//   append (compress_dev.cuh, also fused into the attention launch)  one warp per token, lane l
+//                           owns channels 4l..4l+3
 // P:62 / P:173 (per-token magnitude pruning of K and V), P:218 (bitmap format)
 // (prefill-then-compress, evict-on-exit), P:441 (multiples-of-8 padding).
 #include "compress_dev.cuh"
@@ -25,27 +29,149 @@ __global__ void set_counters_uniform(int32_t* n_comp, int32_t* n_win, int U, int
   }
 }
 
-// Bulk (prefill) mode: warp job j -> (tensor, unit, token). Counters were set beforehand.
+// Bulk (prefill) mode: four tokens per warp, eight lanes per token (lane r = lane & 7 of
+// token slot q = lane >> 3 owns channels 16r..16r+15: two 16-byte loads, eight registers of
+// two fp16 each). The bisection of a2 is the one of select_keep_nibble, but one warp sum
+// serves the four tokens: each slot's count (<= 128) travels in its own byte of the summed
+// word, so per token and step there is a quarter of a REDUX and a quarter of the fixed
+// compare/select work. Flags (top bit of a field after the SWAR subtract) are moved and
+// accumulated with multiply-high on the FMA pipe; the ALU pipe only masks them.
+// Grid (ceil(T / (8 * 4 * kPrefillGroups)), min(2U, 65535)): row = tensor * U + unit (strided by
+// gridDim.y); warp w of block x handles token groups of 4 starting at (8x + w) * 4 * kPrefillGroups.
+// Control flow is warp-uniform (a token past the row's end computes on zeros and stores nothing).
+constexpr int kPrefillGroups = 4;  // 4-token groups per warp
+__device__ __forceinline__ uint32_t shfl_down8(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d, 8); }
+__device__ __forceinline__ uint32_t shfl_up8(uint32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d, 8); }
+
 __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_t* __restrict__ k,
                                                       const uint16_t* __restrict__ v, int T) {
-  const int lane = threadIdx.x & 31;
-  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long per_tensor = (long long)c.U * T;
-  for (long long job = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); job < 2 * per_tensor;
-       job += nwarps) {
-    const int x = job >= per_tensor;  // 0 = K, 1 = V
-    const long long r = job - x * per_tensor;
-    const int u = (int)(r / T), t = (int)(r % T);
-    const int nc = c.n_comp[u], nw = c.n_win[u];
-    if (t >= nc + nw) continue;
-    const uint16_t* src = (x ? v : k) + ((long long)u * T + t) * kD;
+  const int lane = threadIdx.x & 31, q = lane >> 3, r = lane & 7;
+  // byte_perm selectors: put byte 3 (resp. 2) of a word into byte q, zeros elsewhere; take byte q
+  const uint32_t put3 = (0x4444u & ~(0xFu << (4 * q))) | (3u << (4 * q));
+  const uint32_t put2 = (0x4444u & ~(0xFu << (4 * q))) | (2u << (4 * q));
+  const uint32_t take = 0x4440u | (uint32_t)q;
+  for (int row = blockIdx.y; row < 2 * c.U; row += gridDim.y) {
+    const int x = row >= c.U;  // 0 = K, 1 = V
+    const int u = row - x * c.U;
+    const int nc = c.n_comp[u], nw = c.n_win[u], ntok = nc + nw;
+    const int g0 = ((int)blockIdx.x * 8 + (int)(threadIdx.x >> 5)) * 4 * kPrefillGroups;
+    if (g0 >= ntok) continue;
     const Sel z = sel_tensor(c, x);
-    if (t < nc) {
-      const size_t rec = (size_t)u * c.cap + t;
-      compress_token_warp(src, z.keep, z.kpad, (uint32_t)t, z.bm + rec * kTiles, z.val + rec * z.kpad,
-                          z.off + rec * kTiles, lane);
-    } else {
-      copy_token_warp(src, z.win + ((size_t)u * c.W + (t % c.W)) * kD, lane);
+    const uint32_t kk = (uint32_t)z.keep;
+    const uint4* src = reinterpret_cast<const uint4*>((x ? v : k) + (size_t)u * T * kD) + 2 * r;
+    const int gend = min(g0 + 4 * kPrefillGroups, ntok);
+    uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+    if (g0 + q < gend) {
+      n0 = __ldcs(src + (size_t)(g0 + q) * (kD / 8));
+      n1 = __ldcs(src + (size_t)(g0 + q) * (kD / 8) + 1);
+    }
+    for (int gt = g0; gt < gend; gt += 4) {
+      const int t = gt + q;
+      const bool valid = t < gend;
+      const uint32_t w[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+      if (gt + 4 + q < gend) {
+        n0 = __ldcs(src + (size_t)(gt + 4 + q) * (kD / 8));
+        n1 = __ldcs(src + (size_t)(gt + 4 + q) * (kD / 8) + 1);
+      }
+      if (t >= nc) {  // dense window row (ring slot t % W)
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(z.win + ((size_t)u * c.W + (t % c.W)) * kD) + 2 * r;
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      // ---- a1/a2: tau = max t with #{mag >= t} >= k, per token slot
+      uint32_t ax[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ax[i] = w[i] | 0x80008000u;  // magnitude with the top bit set
+      uint32_t hb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hb[i] = __byte_perm(w[2 * i], w[2 * i + 1], 0x7531) | 0x80808080u;
+      uint32_t t4 = 0;  // bits 14..8 of tau, replicated in 4 bytes
+#pragma unroll
+      for (int b = 6; b >= 0; --b) {
+        const uint32_t c4 = t4 | (0x01010101u << b);
+        uint32_t f = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f = __umulhi((hb[i] - c4) & 0x80808080u, 1u << 25) + f;  // byte counts
+        const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x01010101u, 0, put3)), 0, take);
+        t4 = cnt >= kk ? c4 : t4;
+      }
+      uint32_t t2 = (t4 & 0x7Fu) * 0x01000100u;  // tau, replicated in 2 halves
+#pragma unroll
+      for (int b = 7; b >= 0; --b) {
+        const uint32_t c2 = t2 | (0x00010001u << b);
+        uint32_t f = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f = __umulhi((ax[i] - c2) & 0x80008000u, 1u << 17) + f;  // half counts
+        const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x00010001u, 0, put2)), 0, take);
+        t2 = cnt >= kk ? c2 : t2;
+      }
+      // keep mask of the lane's 16 channels: bit j <-> channel 16r + j (mag >= tau)
+      uint32_t acc = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = __umulhi((ax[i] - t2) & 0x80008000u, 1u << (17 + 2 * i)) + acc;
+      uint32_t m16 = (acc & 0xFFFFu) | (acc >> 15);
+      if (!valid) m16 = 0;
+      const uint32_t ge = __byte_perm(warp_sum(__byte_perm(__popc(m16), 0, 0x4440u) << (8 * q)), 0, take);
+      if (__any_sync(0xffffffffu, valid && ge > kk)) {
+        // ties at tau: keep the (k - #{mag > tau}) highest channel indices among mag == tau (R2)
+        const uint32_t tau = t2 & 0x7FFFu;
+        uint32_t eq = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          eq |= (uint32_t)((w[i] & 0x7FFFu) == tau) << (2 * i);
+          eq |= (uint32_t)(((w[i] >> 16) & 0x7FFFu) == tau) << (2 * i + 1);
+        }
+        if (!valid) eq = 0;
+        const uint32_t gt_mask = m16 & ~eq;
+        const uint32_t ngt = __byte_perm(warp_sum((uint32_t)__popc(gt_mask) << (8 * q)), 0, take);
+        // eq channels in higher lanes of the same token (suffix sum over r)
+        uint32_t above = __popc(eq), incl = above;
+#pragma unroll
+        for (int d = 1; d < 8; d <<= 1) {
+          const uint32_t y = shfl_down8(incl, d);
+          if (r + d < 8) incl += y;
+        }
+        above = incl - above;
+        if (valid && ge > kk) {
+          const uint32_t need = kk - ngt;
+          uint32_t keep_eq = 0;
+#pragma unroll
+          for (int j = 15; j >= 0; --j) {
+            if ((eq >> j) & 1u) {
+              if (above < need) keep_eq |= 1u << j;
+              ++above;
+            }
+          }
+          m16 = gt_mask | keep_eq;
+        }
+      }
+      // ---- a3: bitmap words, packed values, tile offsets
+      const uint32_t pc = __popc(m16);
+      uint32_t pos = pc;  // exclusive prefix over the token's lanes
+#pragma unroll
+      for (int d = 1; d < 8; d <<= 1) {
+        const uint32_t y = shfl_up8(pos, d);
+        if (r >= d) pos += y;
+      }
+      pos -= pc;
+      const uint32_t hi16 = shfl_down8(m16, 1);
+      if (valid && t < nc) {
+        const size_t rec = (size_t)u * c.cap + t;
+        if ((r & 1) == 0) reinterpret_cast<uint32_t*>(z.bm + rec * kTiles)[r >> 1] = m16 | (hi16 << 16);
+        if ((r & 3) == 0) z.off[rec * kTiles + (r >> 2)] = (uint32_t)t * (uint32_t)z.kpad + pos;
+        uint16_t* vo = z.val + rec * z.kpad;
+        uint32_t p = pos;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if ((m16 >> (2 * i)) & 1u) vo[p++] = (uint16_t)(w[i] & 0xFFFFu);
+          if ((m16 >> (2 * i + 1)) & 1u) vo[p++] = (uint16_t)(w[i] >> 16);
+        }
+        if (r == 7) {
+          for (int j = (int)kk; j < z.kpad; ++j) vo[j] = 0;  // zero padding (R7)
+        }
+      }
     }
   }
 }
@@ -82,10 +208,9 @@ cudaError_t launch_set_counters(const CacheView& c, const int32_t* nc_host, cons
 cudaError_t launch_prefill(const CacheView& c, const uint16_t* k, const uint16_t* v, int32_t T,
                            cudaStream_t s) {
   if (T == 0 || c.U == 0) return cudaSuccess;
-  const long long jobs = 2LL * c.U * T;
-  long long blocks = (jobs + 7) / 8;
-  if (blocks > 148LL * 64) blocks = 148LL * 64;
-  prefill_kernel<<<(int)blocks, 256, 0, s>>>(c, k, v, T);
+  const int per_block = 8 * 4 * kPrefillGroups;
+  const dim3 grid((unsigned)((T + per_block - 1) / per_block), (unsigned)min(2 * c.U, 65535));
+  prefill_kernel<<<grid, 256, 0, s>>>(c, k, v, T);
   return cudaGetLastError();
 }
 

@@ -9,68 +9,123 @@
 
 namespace mstf {
 
-// Compress one fp16 token vector `src` (device, 8B-aligned, kD halves) into record `rec`.
-__device__ __forceinline__ void compress_token_warp(const uint16_t* __restrict__ src, int k, int kpad,
-                                                    uint32_t rec, uint64_t* __restrict__ bm_out,
-                                                    uint16_t* __restrict__ val_out,
-                                                    uint32_t* __restrict__ off_out, int lane) {
-  const uint2 raw = *reinterpret_cast<const uint2*>(src + 4 * lane);
-  uint32_t h[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
-  uint32_t m[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) m[j] = h[j] & 0x7FFFu;
+// Warp-wide u32 reductions as inline PTX: every caller reaches them with the whole warp
+// converged (warp-uniform control flow), and the intrinsics' divergence-safe lowering
+// (WARPSYNC.COLLECTIVE around each REDUX) cost the old prefill kernel most of its time.
+__device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
+  uint32_t r;
+  asm volatile("redux.sync.add.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t warp_or(uint32_t x) {
+  uint32_t r;
+  asm volatile("redux.sync.or.b32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(x));
+  return r;
+}
 
-  // tau = max t such that #{c : mag_c >= t} >= k   (count is non-increasing in t)
-  uint32_t tau = 0;
+// Top-k selection of one token vector (a1, a2): lane l holds channels 4l..4l+3 as raw fp16
+// bits (x: channels 4l, 4l+1; y: 4l+2, 4l+3). Returns the lane's 4-bit keep nibble (bit j <->
+// channel 4l+j). Exactly k bits are set over the warp.
+//   tau = max t such that #{c : mag_c >= t} >= k, found MSB-first. SWAR compares: with the
+//   top bit of each field set, (field | top) - cand keeps the top bit iff field >= cand and
+//   never borrows across fields. Bits 14..8 compare the high bytes (4 per register), bits
+//   7..0 the full 15-bit magnitudes (2 per register).
+//   Ties at tau (only when #{mag >= tau} > k): keep the (k - #{mag > tau}) highest channel
+//   indices among mag == tau (R2: the lower index is pruned first).
+__device__ __forceinline__ uint32_t select_keep_nibble(uint32_t x, uint32_t y, uint32_t k, int lane) {
+  const uint32_t mx = x & 0x7FFF7FFFu, my = y & 0x7FFF7FFFu;
+  // phase 1: bits 14..8 on the high bytes of the four magnitudes. The lane's flags (top bit
+  // of each byte) move to bit 0 of their bytes with a multiply-high and are summed into the
+  // top byte with a multiply, both on the FMA pipe; the warp sum of that byte (<= 128; the
+  // lower bytes never carry into it) is compared against k << 24.
+  const uint32_t hb = __byte_perm(mx, my, 0x7531) | 0x80808080u;
+  const uint32_t k24 = k << 24, k16 = k << 16;
+  uint32_t t4 = 0;  // tau >> 8, replicated in 4 bytes
 #pragma unroll
-  for (int b = 14; b >= 0; --b) {
-    const uint32_t cand = tau | (1u << b);
-    uint32_t c = (m[0] >= cand) + (m[1] >= cand) + (m[2] >= cand) + (m[3] >= cand);
-    c = __reduce_add_sync(0xffffffffu, c);
-    if (c >= (uint32_t)k) tau = cand;
+  for (int b = 6; b >= 0; --b) {
+    const uint32_t c4 = t4 | (0x01010101u << b);
+    const uint32_t f = __umulhi((hb - c4) & 0x80808080u, 1u << 25) * 0x01010101u;
+    t4 = warp_sum(f) >= k24 ? c4 : t4;
   }
-  uint32_t gt = (m[0] > tau) + (m[1] > tau) + (m[2] > tau) + (m[3] > tau);
-  gt = __reduce_add_sync(0xffffffffu, gt);
-  const uint32_t need = (uint32_t)k - gt;  // >= 1 slots for channels with mag == tau
-
-  // ties: keep the `need` highest channel indices among mag == tau
-  const uint32_t gtm = lanemask_gt();
-  uint32_t above = 0;
-  bool eq[4];
+  // phase 2: bits 7..0 on the 15-bit magnitudes (flags at bits 0 and 16, summed into the
+  // upper half)
+  const uint32_t ax = mx | 0x80008000u, ay = my | 0x80008000u;
+  uint32_t t2 = (t4 & 0x7Fu) * 0x01000100u;  // tau, replicated in 2 halves
+#pragma unroll
+  for (int b = 7; b >= 0; --b) {
+    const uint32_t c2 = t2 | (0x00010001u << b);
+    const uint32_t f = (__umulhi((ax - c2) & 0x80008000u, 1u << 17) + __umulhi((ay - c2) & 0x80008000u, 1u << 17)) *
+                       0x00010001u;
+    t2 = warp_sum(f) >= k16 ? c2 : t2;
+  }
+  const uint32_t tau = t2 & 0x7FFFu;
+  const uint32_t m[4] = {mx & 0xFFFFu, mx >> 16, my & 0xFFFFu, my >> 16};
+  uint32_t nib = 0, ge = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    eq[j] = (m[j] == tau);
-    above += __popc(__ballot_sync(0xffffffffu, eq[j]) & gtm);
+    nib |= (uint32_t)(m[j] >= tau) << j;
+    ge += m[j] >= tau;
   }
-  uint32_t nib = 0;
+  ge = warp_sum(ge);
+  if (ge > k) {  // warp-uniform: ties at tau
+    uint32_t gt = 0;
 #pragma unroll
-  for (int j = 3; j >= 0; --j) {
-    const bool keep = (m[j] > tau) || (eq[j] && above < need);
-    if (eq[j]) ++above;
-    nib |= (uint32_t)keep << j;
+    for (int j = 0; j < 4; ++j) gt += m[j] > tau;
+    const uint32_t need = k - warp_sum(gt);  // >= 1 slots for channels with mag == tau
+    const uint32_t gtm = lanemask_gt();
+    uint32_t above = 0;
+    bool eq[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      eq[j] = (m[j] == tau);
+      above += __popc(__ballot_sync(0xffffffffu, eq[j]) & gtm);
+    }
+    nib = 0;
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+      const bool keep = (m[j] > tau) || (eq[j] && above < need);
+      if (eq[j]) ++above;
+      nib |= (uint32_t)keep << j;
+    }
   }
+  return nib;
+}
 
+// Compress one fp16 token vector (raw = this lane's 4 channels, already loaded) into record
+// `rec` (a3): bitmaps, packed values + zero padding, tile offsets.
+__device__ __forceinline__ void compress_raw_warp(uint2 raw, int k, int kpad, uint32_t rec,
+                                                  uint64_t* __restrict__ bm_out, uint16_t* __restrict__ val_out,
+                                                  uint32_t* __restrict__ off_out, int lane) {
+  const uint32_t nib = select_keep_nibble(raw.x, raw.y, (uint32_t)k, lane);
   // 128-bit keep mask: word i = channels 32i..32i+31 = lanes 8i..8i+7
   const int wi = lane >> 3, sh = 4 * (lane & 7);
   uint32_t w[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) w[i] = __reduce_or_sync(0xffffffffu, wi == i ? (nib << sh) : 0u);
-
+  for (int i = 0; i < 4; ++i) w[i] = warp_or(wi == i ? (nib << sh) : 0u);
   const uint32_t wsel = wi == 0 ? w[0] : wi == 1 ? w[1] : wi == 2 ? w[2] : w[3];
   uint32_t pos = __popc(wsel & ((1u << sh) - 1u));
 #pragma unroll
   for (int i = 0; i < 3; ++i) pos += (i < wi) ? __popc(w[i]) : 0u;
+  const uint32_t h[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (nib & (1u << j)) val_out[pos++] = (uint16_t)h[j];
   }
   if (lane < kpad - k) val_out[k + lane] = 0;  // zero padding
   if (lane == 0) {
-    const uint4 bmw = make_uint4(w[0], w[1], w[2], w[3]);
-    *reinterpret_cast<uint4*>(bm_out) = bmw;  // little endian: tile0 = w0 | w1 << 32
+    *reinterpret_cast<uint4*>(bm_out) = make_uint4(w[0], w[1], w[2], w[3]);  // tile0 = w0 | w1 << 32
     const uint32_t base = rec * (uint32_t)kpad;
     *reinterpret_cast<uint2*>(off_out) = make_uint2(base, base + __popc(w[0]) + __popc(w[1]));
   }
+}
+
+// Compress one fp16 token vector `src` (device, 8B-aligned, kD halves) into record `rec`.
+__device__ __forceinline__ void compress_token_warp(const uint16_t* __restrict__ src, int k, int kpad,
+                                                    uint32_t rec, uint64_t* __restrict__ bm_out,
+                                                    uint16_t* __restrict__ val_out,
+                                                    uint32_t* __restrict__ off_out, int lane) {
+  const uint2 raw = *reinterpret_cast<const uint2*>(src + 4 * lane);
+  compress_raw_warp(raw, k, kpad, rec, bm_out, val_out, off_out, lane);
 }
 
 __device__ __forceinline__ void copy_token_warp(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
