@@ -23,6 +23,10 @@ What it computes:
   * attention           Algorithm 1 in float64: scores over the compressed
                         and window tokens, one softmax over the concatenation, P.V (R10, R11)
   * size_model_paper    byte accounting of the paper's format orientation
+  * query_abs_sum       output-aware accumulator w = sum over the window's queries and the
+                        GQA group of |Q| (R21), float32 in a fixed order
+  * key_scores,         per-token output-aware Key pruning: S = |K| * broadcast(w), top-k of
+    prune_tokens_scored S per token, lower index pruned first on ties (R20)
 
 Pins (tests/test_oracle*.py, `-m "not gpu"`): closed forms, the SPEC worked examples,
 brute-force rank counting and exhaustive subsets on tiny inputs, the lossless round
@@ -40,6 +44,7 @@ __all__ = [
     "keep_count", "k_pad_of", "magnitude", "prune_tokens", "apply_keep",
     "compress_tokens", "decompress_tokens", "FormatError", "OracleCache",
     "attention", "attention_dense", "size_model_paper", "size_model_build",
+    "query_abs_sum", "key_scores", "prune_tokens_scored",
 ]
 
 
@@ -86,6 +91,54 @@ def prune_tokens(bits: np.ndarray, k: int) -> np.ndarray:
     keep = np.ones(bits.shape, dtype=bool)
     pruned = order[..., : d - k]
     np.put_along_axis(keep, pruned, False, axis=-1)
+    return keep
+
+
+def query_abs_sum(q_ring: np.ndarray) -> np.ndarray:
+    """Output-aware accumulator (P:86 'the element-wise L1 accumulation of the current and
+    next 31 Query vector'; P:93 'For GQA ... we sum the pruning score of all queries mapped
+    to each KV cache').
+
+    q_ring: uint16 fp16 bit patterns [U, R, G, d]: the R queries of the window (slot order) of
+    each unit's G query heads. Returns float32 [U, d]: w[u, c] = sum_r sum_g |q[u, r, g, c]|.
+
+    R21: float32, added one term at a time in the order r ascending, then g ascending (the
+    kernel's precision and order, so both sides hold the same bits)."""
+    q = np.asarray(q_ring, dtype=np.uint16)
+    U, R, G, d = q.shape
+    a = np.abs(q.view(np.float16).astype(np.float32))
+    w = np.zeros((U, d), dtype=np.float32)
+    for r in range(R):
+        for g in range(G):
+            w = (w + a[:, r, g, :]).astype(np.float32)   # one float32 add per term
+    return w
+
+
+def key_scores(bits: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """Per-token output-aware Key score S = |K| (.) broadcast(w). bits: uint16 [..., d]
+    fp16 token vectors; w: float32 [d] (or broadcastable), finite and >= 0.
+
+    R20: |K| is the fp16 magnitude widened exactly to float32; the product is one float32
+    multiply, rounded to nearest (the kernel's precision)."""
+    k = np.abs(np.asarray(bits, dtype=np.uint16).view(np.float16).astype(np.float32))
+    return (k * np.asarray(w, dtype=np.float32)).astype(np.float32)
+
+
+def prune_tokens_scored(scores: np.ndarray, k: int) -> np.ndarray:
+    """Keep the k largest scores per row (P:91 'The absolute value of the score element ...
+    is used to decide the elements to be pruned within a token's Key vector'); scores are
+    >= 0, so |S| = S. Ties: the lower channel index is pruned first (R2), as in prune_tokens.
+    Returns bool keep mask with exactly k True per row."""
+    sc = np.asarray(scores, dtype=np.float32)
+    d = sc.shape[-1]
+    if not (1 <= k <= d):
+        raise ValueError("k must be in [1, d]")
+    if np.isnan(sc).any() or (sc < 0).any():
+        raise ValueError("scores must be >= 0")
+    idx = np.broadcast_to(np.arange(d, dtype=np.int64), sc.shape)
+    order = np.lexsort((idx, sc.astype(np.float64)), axis=-1)
+    keep = np.ones(sc.shape, dtype=bool)
+    np.put_along_axis(keep, order[..., : d - k], False, axis=-1)
     return keep
 
 
@@ -193,13 +246,23 @@ class OracleCache:
         self.win_v = z((U, max(window, 1), d), np.uint16)
         self.n_comp = z(U, np.int64)
         self.n_win = z(U, np.int64)
+        self.key_weights = None   # float32 [U, d]: output-aware K pruning when set
+
+    def set_key_weights(self, w):
+        """Output-aware K pruning for every later K compression (prefill and evictions) with
+        S = |K| * w[u] (key_scores); None restores magnitude pruning. V is always pruned by
+        magnitude (per-token magnitude is already output-aware for V)."""
+        self.key_weights = None if w is None else np.asarray(w, dtype=np.float32).copy()
 
     # -- one tensor, one unit: compress tokens (given as bits) into records r0..r0+T-1
     def _store(self, which: str, u: int, r0: int, bits: np.ndarray):
         k = self.kk if which == "k" else self.kv
         if r0 + bits.shape[0] > self.cap:
             raise OverflowError("compressed capacity exceeded")
-        keep = prune_tokens(bits, k)
+        if which == "k" and self.key_weights is not None:
+            keep = prune_tokens_scored(key_scores(bits, self.key_weights[u]), k)
+        else:
+            keep = prune_tokens(bits, k)
         bm, vals, offs = compress_tokens(bits, keep, k, first_record=r0)
         getattr(self, "bitmap_" + which)[u, r0:r0 + len(bits)] = bm
         getattr(self, "values_" + which)[u, r0:r0 + len(bits)] = vals

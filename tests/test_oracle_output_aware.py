@@ -1,0 +1,135 @@
+"""Pins of the output-aware Key pruning oracle (NEXT-2): query_abs_sum, key_scores,
+prune_tokens_scored and OracleCache with key weights. CPU only (-m "not gpu").
+
+Each pin ties the oracle to something other than itself: SPEC's worked accumulator example,
+hand-computed scores, brute-force rank counting and exhaustive subsets on tiny rows, exact
+reductions to magnitude pruning (weights that are all one or one power of two change no
+comparison), and an fp64 sum where the float32 sum is exact.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import mustafar_oracle as O
+
+
+def bits_of(vals):
+    return np.asarray(vals, dtype=np.float16).view(np.uint16)
+
+
+# ----------------------------------------------------------------------------- accumulator
+def test_query_abs_sum_spec_gqa_example():
+    """a GQA group of 2 query heads, each query [1, 0] -> acc [2, 0] after one step."""
+    q = bits_of([[[[1.0, 0.0], [1.0, 0.0]]]])          # [U=1, R=1, G=2, d=2]
+    assert O.query_abs_sum(q).tolist() == [[2.0, 0.0]]
+
+
+def test_query_abs_sum_signs_and_zero_query():
+    """L1 accumulation: signs are dropped (P:86 'L1'); a zero query adds nothing."""
+    q = bits_of([[[[-1.5, 2.0, -0.0]], [[0.0, 0.0, 0.0]], [[0.25, -3.0, 1.0]]]])  # [1, 3, 1, 3]
+    assert O.query_abs_sum(q).tolist() == [[1.75, 5.0, 1.0]]
+
+
+def test_query_abs_sum_matches_fp64_when_exact():
+    """Small dyadic values: every float32 partial sum is exact, so the result equals the
+    plain float64 sum of |q| over the window and the group."""
+    rng = np.random.default_rng(1)
+    vals = rng.integers(-64, 65, size=(3, 32, 4, 128)).astype(np.float16) * np.float16(0.125)
+    w = O.query_abs_sum(vals.view(np.uint16))
+    ref = np.abs(vals.astype(np.float64)).sum(axis=(1, 2))
+    assert np.array_equal(w.astype(np.float64), ref)
+
+
+# ----------------------------------------------------------------------------- scores
+def test_key_scores_hand_example():
+    """S = |K| (.) w: |[1, -2, 3, -4]| * [4, 1, 1, 0.5] = [4, 2, 3, 2]; keep 2 ->
+    channels 0 and 2, where magnitude pruning keeps 2 and 3."""
+    b = bits_of([1, -2, 3, -4])
+    w = np.array([4, 1, 1, 0.5], np.float32)
+    s = O.key_scores(b, w)
+    assert s.tolist() == [4.0, 2.0, 3.0, 2.0]
+    assert O.prune_tokens_scored(s, 2).tolist() == [True, False, True, False]
+    assert O.prune_tokens(b, 2).tolist() == [False, False, True, True]
+
+
+def test_scored_tie_rule():
+    """Equal scores: the lower channel index is pruned first (R2): scores [2, 2, 2, 1], k=2
+    keeps channels 1 and 2."""
+    assert O.prune_tokens_scored(np.array([2, 2, 2, 1], np.float32), 2).tolist() == [False, True, True, False]
+
+
+def _brute_keep_scores(sc, k):
+    d = len(sc)
+    return [sum(1 for c2 in range(d) if (sc[c2], c2) > (sc[c], c)) < k for c in range(d)]
+
+
+@pytest.mark.parametrize("kind", ["normal", "lattice", "zeros"])
+@pytest.mark.parametrize("k", [1, 39, 64, 128])
+def test_scored_prune_matches_bruteforce_rank(kind, k):
+    X = synth.fp16_np((16, 128), synth.seed_for(11, k), kind).view(np.uint16)
+    w = np.abs(synth.fp16_np((128,), synth.seed_for(11, 100 + k)).astype(np.float32)) * np.float32(3)
+    S = O.key_scores(X, w)
+    keep = O.prune_tokens_scored(S, k)
+    assert (keep.sum(axis=1) == k).all()
+    for t in range(X.shape[0]):
+        assert keep[t].tolist() == _brute_keep_scores(S[t].tolist(), k)
+
+
+def test_scored_prune_exhaustive_subsets_d8():
+    """The kept set maximises the sum of scores over all k-subsets, and every kept channel
+    beats every pruned one under (score, index)."""
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        b = (rng.integers(-3, 4, size=8).astype(np.float16) * np.float16(0.5)).view(np.uint16)
+        w = rng.integers(0, 4, size=8).astype(np.float32)
+        k = int(rng.integers(1, 9))
+        s = O.key_scores(b, w)
+        keep = O.prune_tokens_scored(s, k)
+        best = max(sum(s[list(c)]) for c in itertools.combinations(range(8), k))
+        assert s[keep].sum() == best
+        for c in np.flatnonzero(keep):
+            for c2 in np.flatnonzero(~keep):
+                assert (s[c], c) > (s[c2], c2)
+
+
+@pytest.mark.parametrize("scale", [1.0, 0.25, 8.0])
+@pytest.mark.parametrize("kind", ["normal", "lattice", "zeros"])
+def test_uniform_weights_reduce_to_magnitude(scale, kind):
+    """w = c * ones with c a power of two scales every score exactly, so no comparison
+    changes: output-aware pruning equals magnitude pruning."""
+    X = synth.fp16_np((32, 128), synth.seed_for(12, int(scale * 4)), kind).view(np.uint16)
+    w = np.full(128, scale, np.float32)
+    assert np.array_equal(O.prune_tokens_scored(O.key_scores(X, w), 39), O.prune_tokens(X, 39))
+
+
+def test_rejects_negative_scores():
+    with pytest.raises(ValueError):
+        O.prune_tokens_scored(np.array([1.0, -1.0], np.float32), 1)
+
+
+# ----------------------------------------------------------------------------- cache
+def test_cache_key_weights_change_k_only():
+    """With key weights the K records follow prune_tokens_scored, V records stay magnitude
+    pruned; unit weights reproduce the plain cache bit for bit."""
+    U, T, d, W = 2, 80, 128, 32
+    K = synth.fp16_np((U, T, d), 5).view(np.uint16)
+    V = synth.fp16_np((U, T, d), 6).view(np.uint16)
+    w = np.abs(synth.fp16_np((U, d), 7).astype(np.float32))
+    a = O.OracleCache(U, d, 39, 39, W, T)
+    a.set_key_weights(w)
+    a.prefill(K, V)
+    b = O.OracleCache(U, d, 39, 39, W, T)
+    b.prefill(K, V)
+    assert np.array_equal(a.bitmap_v, b.bitmap_v) and np.array_equal(a.values_v, b.values_v)
+    assert not np.array_equal(a.bitmap_k, b.bitmap_k)
+    nc = T - W
+    for u in range(U):
+        keep = O.prune_tokens_scored(O.key_scores(K[u, :nc], w[u]), 39)
+        bm, vals, _ = O.compress_tokens(K[u, :nc], keep, 39)
+        assert np.array_equal(a.bitmap_k[u, :nc], bm) and np.array_equal(a.values_k[u, :nc], vals)
+    c = O.OracleCache(U, d, 39, 39, W, T)
+    c.set_key_weights(np.ones((U, d), np.float32))
+    c.prefill(K, V)
+    assert np.array_equal(c.bitmap_k, b.bitmap_k) and np.array_equal(c.values_k, b.values_k)
