@@ -193,6 +193,27 @@ int mstf_decode_step_kernel_count(const mstf_cache* cache);
  * Host-only; lets callers count launches. */
 int mstf_attention_kernel_count(const mstf_cache* cache);
 
+/* ------------------------------------------------------------------ output-aware Key pruning
+ * Per-token OUTPUT-AWARE pruning of the Key cache:
+ *   S = |K| (.) broadcast(w),  w = sum over the window's queries t of |Q_t|, summed over the
+ *   GQA group's query heads.
+ * mstf_set_key_weights: every later K compression of this cache (mstf_prune_compress_kv,
+ * the evictions of mstf_append_token / mstf_decode_step) keeps, per token, the keep_k channels
+ * with the largest score fl32(|k_c| * w[u][c]) (one float32 multiply, round to nearest, R20),
+ * lower channel index pruned first on equal scores (R2). V stays magnitude pruned.
+ * w: DEVICE float32 [U][head_dim], 16-byte aligned, finite and >= 0, owned by the caller and
+ * read by the kernels at run time (update it in stream order between steps); NULL restores
+ * magnitude pruning. Errors: EINVAL (misaligned).                                       */
+int mstf_set_key_weights(mstf_cache* cache, const float* w);
+
+/* The accumulator of P:86 ("the element-wise L1 accumulation of the current and next 31
+ * Query vector"): w[u][c] = sum_{r < R} sum_{g < G} |q[u][r][g][c]| in float32, added in the
+ * order r ascending, then g ascending (R21). q: fp16 DEVICE [U][R][G][d] (the window's R
+ * queries of each unit's G query heads, in any fixed slot order, e.g. a ring); w: DEVICE
+ * float32 [U][d]. R = 0 gives zeros. Errors: EINVAL (null, negative sizes), ECUDA.          */
+int mstf_query_abs_sum(const void* q, int32_t units, int32_t slots, int32_t group, int32_t head_dim,
+                       float* w, void* stream);
+
 /* Human-readable status (static string). */
 const char* mstf_status_string(int32_t status);
 

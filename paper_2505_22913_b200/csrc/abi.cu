@@ -310,6 +310,22 @@ int mstf_dense_decode_attention(const void* k, const void* v, const int32_t* len
   return MSTF_OK;
 }
 
+int mstf_set_key_weights(mstf_cache* h, const float* w) {
+  if (!h) return MSTF_EINVAL;
+  if (w && !aligned16(w)) return MSTF_EINVAL;
+  h->view.kw = w;
+  return MSTF_OK;
+}
+
+int mstf_query_abs_sum(const void* q, int32_t units, int32_t slots, int32_t group, int32_t head_dim, float* w,
+                       void* stream) {
+  if (units < 0 || slots < 0 || group < 1 || head_dim < 1) return MSTF_EINVAL;
+  if ((long long)units * head_dim > 0 && (!w || (slots > 0 && !q))) return MSTF_EINVAL;
+  const cudaError_t e = launch_query_abs_sum(static_cast<const uint16_t*>(q), units, slots, group, head_dim, w,
+                                             static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MSTF_OK : MSTF_ECUDA;
+}
+
 int mstf_shard_units(int32_t units, int32_t world, int32_t rank, int32_t* u0, int32_t* u1) {
   if (units < 0 || world < 1 || rank < 0 || rank >= world || !u0 || !u1) return MSTF_EINVAL;
   *u0 = (int32_t)((int64_t)units * rank / world);

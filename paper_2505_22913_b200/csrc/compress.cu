@@ -58,8 +58,24 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
     if (g0 >= ntok) continue;
     const Sel z = sel_tensor(c, x);
     const uint32_t kk = (uint32_t)z.keep;
-    const uint4* src = reinterpret_cast<const uint4*>((x ? v : k) + (size_t)u * T * kD) + 2 * r;
     const int gend = min(g0 + 4 * kPrefillGroups, ntok);
+    if (x == 0 && c.kw) {
+      // output-aware K pruning: one warp per token, float32 score keys
+      const float* kw = c.kw + (size_t)u * kD;
+      const uint16_t* base = k + (size_t)u * T * kD;
+      for (int t = g0; t < gend; ++t) {
+        const uint2 raw = reinterpret_cast<const uint2*>(base + (size_t)t * kD)[lane];
+        if (t < nc) {
+          const size_t rec = (size_t)u * c.cap + t;
+          compress_raw_warp(raw, z.keep, z.kpad, (uint32_t)t, z.bm + rec * kTiles, z.val + rec * z.kpad,
+                            z.off + rec * kTiles, lane, kw);
+        } else {
+          reinterpret_cast<uint2*>(z.win + ((size_t)u * c.W + (t % c.W)) * kD)[lane] = raw;
+        }
+      }
+      continue;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>((x ? v : k) + (size_t)u * T * kD) + 2 * r;
     uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
     if (g0 + q < gend) {
       n0 = __ldcs(src + (size_t)(g0 + q) * (kD / 8));
@@ -191,6 +207,28 @@ __global__ void __launch_bounds__(64) append_kernel(CacheView c, const uint16_t*
     else
       c.n_win[u] = nw + 1;
   }
+}
+
+// Output-aware accumulator (R21): w[u][c] = sum_r sum_g |q[u][r][g][c]| in float32,
+// r ascending then g ascending (one thread per (unit, channel); the order the oracle uses).
+__global__ void query_abs_sum_kernel(const uint16_t* __restrict__ q, int U, int R, int G, int d,
+                                     float* __restrict__ w) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)U * d) return;
+  const int u = (int)(i / d), ch = (int)(i % d);
+  const uint16_t* p = q + (size_t)u * R * G * d + ch;
+  float acc = 0.f;
+  for (int r = 0; r < R; ++r)
+    for (int g = 0; g < G; ++g) acc = __fadd_rn(acc, __half2float(__ushort_as_half((unsigned short)(p[((size_t)r * G + g) * d] & 0x7FFFu))));
+  w[i] = acc;
+}
+
+cudaError_t launch_query_abs_sum(const uint16_t* q, int32_t U, int32_t R, int32_t G, int32_t d, float* w,
+                                 cudaStream_t s) {
+  const long long n = (long long)U * d;
+  if (n == 0) return cudaSuccess;
+  query_abs_sum_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(q, U, R, G, d, w);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_set_counters(const CacheView& c, const int32_t* nc_host, const int32_t* nw_host,

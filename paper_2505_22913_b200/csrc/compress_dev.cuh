@@ -23,6 +23,41 @@ __device__ __forceinline__ uint32_t warp_or(uint32_t x) {
   return r;
 }
 
+// Keep nibble for keys m[4] (lane l: channels 4l..4l+3) given tau = the k-th largest key:
+// keys > tau are kept; among keys == tau the (k - #{key > tau}) highest channel indices (R2:
+// the lower index is pruned first). Warp-uniform control flow.
+__device__ __forceinline__ uint32_t keep_nibble_at(const uint32_t (&m)[4], uint32_t tau, uint32_t k) {
+  uint32_t nib = 0, ge = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    nib |= (uint32_t)(m[j] >= tau) << j;
+    ge += m[j] >= tau;
+  }
+  ge = warp_sum(ge);
+  if (ge > k) {  // warp-uniform: ties at tau
+    uint32_t gt = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gt += m[j] > tau;
+    const uint32_t need = k - warp_sum(gt);  // >= 1 slots for channels with key == tau
+    const uint32_t gtm = lanemask_gt();
+    uint32_t above = 0;
+    bool eq[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      eq[j] = (m[j] == tau);
+      above += __popc(__ballot_sync(0xffffffffu, eq[j]) & gtm);
+    }
+    nib = 0;
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+      const bool keep = (m[j] > tau) || (eq[j] && above < need);
+      if (eq[j]) ++above;
+      nib |= (uint32_t)keep << j;
+    }
+  }
+  return nib;
+}
+
 // Top-k selection of one token vector (a1, a2): lane l holds channels 4l..4l+3 as raw fp16
 // bits (x: channels 4l, 4l+1; y: 4l+2, 4l+3). Returns the lane's 4-bit keep nibble (bit j <->
 // channel 4l+j). Exactly k bits are set over the warp.
@@ -60,43 +95,37 @@ __device__ __forceinline__ uint32_t select_keep_nibble(uint32_t x, uint32_t y, u
   }
   const uint32_t tau = t2 & 0x7FFFu;
   const uint32_t m[4] = {mx & 0xFFFFu, mx >> 16, my & 0xFFFFu, my >> 16};
-  uint32_t nib = 0, ge = 0;
+  return keep_nibble_at(m, tau, k);
+}
+
+// Output-aware variant (R20): keys are the float32 scores |x_c| * w_c (non-negative,
+// so their bit patterns order like the values); tau by a 31-step MSB-first search.
+__device__ __forceinline__ uint32_t select_keep_nibble_scored(uint32_t x, uint32_t y, float4 w, uint32_t k) {
+  const uint32_t hv[4] = {x & 0x7FFFu, (x >> 16) & 0x7FFFu, y & 0x7FFFu, (y >> 16) & 0x7FFFu};
+  const float wv[4] = {w.x, w.y, w.z, w.w};
+  uint32_t m[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    nib |= (uint32_t)(m[j] >= tau) << j;
-    ge += m[j] >= tau;
+  for (int j = 0; j < 4; ++j) m[j] = __float_as_uint(__fmul_rn(__half2float(__ushort_as_half((unsigned short)hv[j])), wv[j]));
+  uint32_t tau = 0;
+#pragma unroll 1
+  for (int b = 30; b >= 0; --b) {
+    const uint32_t cand = tau | (1u << b);
+    const uint32_t n = warp_sum((uint32_t)(m[0] >= cand) + (uint32_t)(m[1] >= cand) + (uint32_t)(m[2] >= cand) +
+                                (uint32_t)(m[3] >= cand));
+    tau = n >= k ? cand : tau;
   }
-  ge = warp_sum(ge);
-  if (ge > k) {  // warp-uniform: ties at tau
-    uint32_t gt = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) gt += m[j] > tau;
-    const uint32_t need = k - warp_sum(gt);  // >= 1 slots for channels with mag == tau
-    const uint32_t gtm = lanemask_gt();
-    uint32_t above = 0;
-    bool eq[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      eq[j] = (m[j] == tau);
-      above += __popc(__ballot_sync(0xffffffffu, eq[j]) & gtm);
-    }
-    nib = 0;
-#pragma unroll
-    for (int j = 3; j >= 0; --j) {
-      const bool keep = (m[j] > tau) || (eq[j] && above < need);
-      if (eq[j]) ++above;
-      nib |= (uint32_t)keep << j;
-    }
-  }
-  return nib;
+  return keep_nibble_at(m, tau, k);
 }
 
 // Compress one fp16 token vector (raw = this lane's 4 channels, already loaded) into record
 // `rec` (a3): bitmaps, packed values + zero padding, tile offsets.
+// kw: this unit's float32 channel weights for output-aware K pruning, or null (magnitude).
 __device__ __forceinline__ void compress_raw_warp(uint2 raw, int k, int kpad, uint32_t rec,
                                                   uint64_t* __restrict__ bm_out, uint16_t* __restrict__ val_out,
-                                                  uint32_t* __restrict__ off_out, int lane) {
-  const uint32_t nib = select_keep_nibble(raw.x, raw.y, (uint32_t)k, lane);
+                                                  uint32_t* __restrict__ off_out, int lane,
+                                                  const float* __restrict__ kw = nullptr) {
+  const uint32_t nib = kw ? select_keep_nibble_scored(raw.x, raw.y, reinterpret_cast<const float4*>(kw)[lane], (uint32_t)k)
+                          : select_keep_nibble(raw.x, raw.y, (uint32_t)k, lane);
   // 128-bit keep mask: word i = channels 32i..32i+31 = lanes 8i..8i+7
   const int wi = lane >> 3, sh = 4 * (lane & 7);
   uint32_t w[4];
@@ -123,9 +152,10 @@ __device__ __forceinline__ void compress_raw_warp(uint2 raw, int k, int kpad, ui
 __device__ __forceinline__ void compress_token_warp(const uint16_t* __restrict__ src, int k, int kpad,
                                                     uint32_t rec, uint64_t* __restrict__ bm_out,
                                                     uint16_t* __restrict__ val_out,
-                                                    uint32_t* __restrict__ off_out, int lane) {
+                                                    uint32_t* __restrict__ off_out, int lane,
+                                                    const float* __restrict__ kw = nullptr) {
   const uint2 raw = *reinterpret_cast<const uint2*>(src + 4 * lane);
-  compress_raw_warp(raw, k, kpad, rec, bm_out, val_out, off_out, lane);
+  compress_raw_warp(raw, k, kpad, rec, bm_out, val_out, off_out, lane, kw);
 }
 
 __device__ __forceinline__ void copy_token_warp(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
@@ -155,13 +185,14 @@ __device__ __forceinline__ void append_unit_warp(const CacheView& c, int x, int 
                                                  int nc, int nw, int lane) {
   const size_t rec = (size_t)u * c.cap + nc;
   const Sel z = sel_tensor(c, x);
+  const float* kw = (x == 0 && c.kw) ? c.kw + (size_t)u * kD : nullptr;
   if (c.W == 0) {
     compress_token_warp(src, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.val + rec * z.kpad,
-                        z.off + rec * kTiles, lane);
+                        z.off + rec * kTiles, lane, kw);
   } else if (nw == c.W) {
     uint16_t* slot = z.win + ((size_t)u * c.W + (nc % c.W)) * kD;
     compress_token_warp(slot, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.val + rec * z.kpad,
-                        z.off + rec * kTiles, lane);
+                        z.off + rec * kTiles, lane, kw);
     __syncwarp();
     copy_token_warp(src, slot, lane);
   } else {

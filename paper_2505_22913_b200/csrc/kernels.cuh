@@ -51,12 +51,15 @@ struct CacheView {
   int32_t* n_win;       // [U]
   int32_t U, W, cap;
   int32_t keep[2], kpad[2];
+  const float* kw;      // [U][kD] float32 K channel weights (output-aware pruning), or null
 };
 
 cudaError_t launch_set_counters(const CacheView& c, const int32_t* nc_host, const int32_t* nw_host,
                                 int32_t uniform_T, cudaStream_t s);
 cudaError_t launch_prefill(const CacheView& c, const uint16_t* k, const uint16_t* v, int32_t T,
                            cudaStream_t s);
+cudaError_t launch_query_abs_sum(const uint16_t* q, int32_t U, int32_t R, int32_t G, int32_t d, float* w,
+                                 cudaStream_t s);
 cudaError_t launch_append(const CacheView& c, const uint16_t* k_new, const uint16_t* v_new,
                           cudaStream_t s);
 

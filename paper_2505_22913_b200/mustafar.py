@@ -29,6 +29,7 @@ EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "
            "mstf_workspace_bytes", "mstf_sparse_decode_attention", "mstf_dense_workspace_bytes",
            "mstf_dense_decode_attention", "mstf_shard_units", "mstf_decode_step",
            "mstf_decode_step_kernel_count", "mstf_attention_kernel_count",
+           "mstf_set_key_weights", "mstf_query_abs_sum",
            "mstf_status_string", "mstf_build_info")
 
 
@@ -73,6 +74,8 @@ def lib() -> ctypes.CDLL:
         "mstf_decode_step": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_float, vp, i32, vp, sz, vp]),
         "mstf_decode_step_kernel_count": (ctypes.c_int, [vp]),
         "mstf_attention_kernel_count": (ctypes.c_int, [vp]),
+        "mstf_set_key_weights": (ctypes.c_int, [vp, vp]),
+        "mstf_query_abs_sum": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, vp]),
         "mstf_status_string": (ctypes.c_char_p, [i32]),
         "mstf_build_info": (ctypes.c_char_p, []),
     }
@@ -114,6 +117,17 @@ def shard_units(units: int, world: int, rank: int):
     a, b = ctypes.c_int32(), ctypes.c_int32()
     _check("mstf_shard_units", lib().mstf_shard_units(units, world, rank, ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
+
+
+def query_abs_sum(q: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Output-aware accumulator: q fp16 [U, R, G, d] (R window queries of each unit's
+    G query heads) -> float32 [U, d], w = sum_r sum_g |q| (mstf_query_abs_sum)."""
+    U, R, G, d = q.shape
+    if out is None:
+        out = torch.empty(U, d, dtype=torch.float32, device=q.device)
+    _check("mstf_query_abs_sum", lib().mstf_query_abs_sum(_dev_ptr(q, name="q"), U, R, G, d,
+                                                          _dev_ptr(out, torch.float32, "out"), _stream(stream)))
+    return out
 
 
 def buffer_bytes(cfg: Config):
@@ -220,6 +234,14 @@ class MustafarCache:
         _check("mstf_prune_compress_kv",
                lib().mstf_prune_compress_kv(self._h, _dev_ptr(k, name="k"), _dev_ptr(v, name="v"), T, ln,
                                             _stream(stream)))
+
+    def set_key_weights(self, w: torch.Tensor | None):
+        """Output-aware K pruning for later K compressions: w float32 [U, d] on the device
+        (read by the kernels at run time; keep it alive and update it in stream order), or None
+        for magnitude pruning (mstf_set_key_weights)."""
+        ptr = None if w is None else _dev_ptr(w, torch.float32, "w")
+        _check("mstf_set_key_weights", lib().mstf_set_key_weights(self._h, ptr))
+        self._kw = w
 
     def append_token(self, k_new: torch.Tensor, v_new: torch.Tensor, stream=None):
         """k_new, v_new: fp16 [U, d] (== [B, Hkv, d]) on the device."""

@@ -105,6 +105,14 @@ def test_host_validation_before_launch(L):
         assert L.mstf_sparse_decode_attention(h, q, 0.1, q, 7, ctypes.c_void_p(0x3000), ws, None) == -1
         nc, nw = (ctypes.c_int32 * 4)(), (ctypes.c_int32 * 4)()
         assert L.mstf_cache_counts(h, nc, nw) == 0 and list(nc) == [0] * 4 and list(nw) == [0] * 4
+        # output-aware key weights: 16-byte alignment, NULL resets; accumulator argument checks
+        assert L.mstf_set_key_weights(h, ctypes.c_void_p(0x1004)) == -1
+        assert L.mstf_set_key_weights(h, ctypes.c_void_p(0x1000)) == 0
+        assert L.mstf_set_key_weights(h, None) == 0
+        assert L.mstf_set_key_weights(None, None) == -1
+        assert L.mstf_query_abs_sum(None, 4, 32, 4, 128, ctypes.c_void_p(0x1000), None) == -1
+        assert L.mstf_query_abs_sum(ctypes.c_void_p(0x1000), 4, 32, 0, 128, ctypes.c_void_p(0x1000), None) == -1
+        assert L.mstf_query_abs_sum(ctypes.c_void_p(0x1000), -1, 32, 4, 128, ctypes.c_void_p(0x1000), None) == -1
     finally:
         L.mstf_cache_destroy(h)
 
