@@ -25,6 +25,8 @@ What it computes:
   * size_model_paper    byte accounting of the paper's format orientation
   * query_abs_sum       output-aware accumulator w = sum over the window's queries and the
                         GQA group of |Q| (R21), float32 in a fixed order
+  * attention_partial,  sequence split across ranks: one shard's softmax
+    merge_partials      partials and their flash-decoding merge
   * key_scores,         per-token output-aware Key pruning: S = |K| * broadcast(w), top-k of
     prune_tokens_scored S per token, lower index pruned first on ties (R20)
 
@@ -44,7 +46,7 @@ __all__ = [
     "keep_count", "k_pad_of", "magnitude", "prune_tokens", "apply_keep",
     "compress_tokens", "decompress_tokens", "FormatError", "OracleCache",
     "attention", "attention_dense", "size_model_paper", "size_model_build",
-    "query_abs_sum", "key_scores", "prune_tokens_scored",
+    "query_abs_sum", "key_scores", "prune_tokens_scored", "attention_partial", "merge_partials",
 ]
 
 
@@ -351,6 +353,45 @@ def attention_regions(qu, kc, vc, kl, vl, scale):
     p = e / e.sum(axis=1, keepdims=True)           # line 3 softmax
     p_c, p_l = p[:, : KC.shape[0]], p[:, KC.shape[0]:]   # line 4 split
     return p_c @ VC + p_l @ VL                     # line 5
+
+
+def attention_partial(cache: OracleCache, q: np.ndarray, scale: float):
+    """One shard's Algorithm 1 stopped before the normalisation of line 3: the
+    softmax partials over this cache's tokens (flash-decoding state), float64,
+    natural-log units:
+      m = max_t s_t,  l = sum_t exp(s_t - m),  o = sum_t exp(s_t - m) v_t
+    with s_t = scale * q . k_t over the compressed and window tokens (R10). Returns (m [U, G],
+    l [U, G], o [U, G, d]); a unit without tokens gives m = -inf, l = 0, o = 0."""
+    U, G, d = cache.U, q.shape[1], cache.d
+    m = np.full((U, G), -np.inf)
+    l = np.zeros((U, G))
+    o = np.zeros((U, G, d))
+    for u in range(U):
+        kc, vc, kl, vl = cache.tokens(u)
+        K = fp16_to_f64(np.concatenate([kc, kl], axis=0))
+        V = fp16_to_f64(np.concatenate([vc, vl], axis=0))
+        if K.shape[0] == 0:
+            continue
+        s = scale * (fp16_to_f64(q[u]) @ K.T)
+        m[u] = s.max(axis=1)
+        e = np.exp(s - m[u][:, None])
+        l[u] = e.sum(axis=1)
+        o[u] = e @ V
+    return m, l, o
+
+
+def merge_partials(parts):
+    """Merge shards' partials [(m, l, o), ...] into O (the a9 split combine; natural units):
+    M = max_i m_i, O = sum_i exp(m_i - M) o_i / sum_i exp(m_i - M) l_i. Shards with m = -inf
+    contribute nothing."""
+    M = np.max(np.stack([p[0] for p in parts]), axis=0)
+    num = np.zeros_like(parts[0][2])
+    den = np.zeros_like(parts[0][1])
+    for m, l, o in parts:
+        w = np.where(np.isneginf(m), 0.0, np.exp(np.where(np.isneginf(m), 0.0, m - M)))
+        num += w[..., None] * o
+        den += w * l
+    return num / den[..., None]
 
 
 def attention_dense(q: np.ndarray, K: np.ndarray, V: np.ndarray, scale: float) -> np.ndarray:
