@@ -193,6 +193,34 @@ int mstf_decode_step_kernel_count(const mstf_cache* cache);
  * Host-only; lets callers count launches. */
 int mstf_attention_kernel_count(const mstf_cache* cache);
 
+/* ------------------------------------------------------------------ sequence split (NEXT-3)
+ * Batch-1 long context has too few units to shard by unit (fewer thread blocks than SMs
+ * at batch 1), so the tokens of every unit are split across ranks instead:
+ * mstf_seq_split: rank r's prompt tokens [t0, t1) of T. The C = T - min(T, W) tokens that are
+ * compressed at prefill are split evenly; the last rank also takes the last min(T, W) tokens (the
+ * dense window, R9), so it alone holds a window (W) and takes every decode append; the other
+ * ranks build their caches with window 0. The union of the shards is exactly the single-device
+ * cache (pruning is per token). Host-only.                                                   */
+int mstf_seq_split(int32_t T, int32_t window, int32_t world, int32_t rank, int32_t* t0, int32_t* t1);
+
+/* Algorithm 1 over this cache's tokens only, stopping before the final normalisation: the
+ * shard's softmax partials (the a9 combine state of flash-decoding), float32 DEVICE:
+ *   ml [U][G][2]: m = max_t s_t*log2(e), l = sum_t 2^(s_t*log2(e) - m);  o [U][G][d]:
+ *   o = sum_t 2^(s_t*log2(e) - m) * v_t (not divided by l), s_t = scale * q . k_t.
+ * q, scale, workspace as in mstf_sparse_decode_attention. ml 8-byte aligned, o 16-byte aligned.
+ * Errors: as mstf_sparse_decode_attention.                                                     */
+int mstf_sparse_decode_attention_partial(const mstf_cache* cache, const void* q, float scale, float* ml,
+                                         float* o, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Merge n shards' partials (e.g. all-gathered across ranks) into the attention output:
+ *   M = max_i m_i,  O = sum_i 2^(m_i - M) o_i / sum_i 2^(m_i - M) l_i       (the a9 combine)
+ * ml: float32 DEVICE [n][units][group][2], o: [n][units][group][head_dim]; out: [units][group]
+ * [head_dim] float32 or fp16 (out_dtype). A shard without tokens (m = -inf) contributes nothing;
+ * a (unit, head) with no token in any shard gives 0. Errors: EINVAL, ENOTSUP (head_dim != 128,
+ * group > 8), ECUDA.                                                                            */
+int mstf_merge_partials(int32_t n, int32_t units, int32_t group, int32_t head_dim, const float* ml,
+                        const float* o, void* out, int32_t out_dtype, void* stream);
+
 /* ------------------------------------------------------------------ output-aware Key pruning
  * Per-token OUTPUT-AWARE pruning of the Key cache:
  *   S = |K| (.) broadcast(w),  w = sum over the window's queries t of |Q_t|, summed over the

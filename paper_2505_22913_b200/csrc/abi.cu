@@ -229,6 +229,31 @@ int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale
   return MSTF_OK;
 }
 
+int mstf_sparse_decode_attention_partial(const mstf_cache* h, const void* q, float scale, float* ml, float* o,
+                                         void* ws, size_t ws_bytes, void* stream) {
+  const int st = check_attention_args(h, q, ml, MSTF_OUT_F32, ws, ws_bytes);
+  if (st != MSTF_OK) return st;
+  if (!o || !aligned16(o) || (reinterpret_cast<uintptr_t>(ml) & 7u)) return MSTF_EINVAL;
+  AttnPlan plan;
+  const int sp = make_plan(h, h->nc, h->nw, &plan);
+  if (sp != MSTF_OK) return sp;
+  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
+  if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, nullptr, 0, ws,
+                              static_cast<cudaStream_t>(stream), nullptr, ml, o) != cudaSuccess)
+    return MSTF_ECUDA;
+  return MSTF_OK;
+}
+
+int mstf_merge_partials(int32_t n, int32_t units, int32_t group, int32_t head_dim, const float* ml, const float* o,
+                        void* out, int32_t out_dtype, void* stream) {
+  if (n < 1 || units < 0 || group < 1 || !ml || !o || !out) return MSTF_EINVAL;
+  if (out_dtype != MSTF_OUT_F32 && out_dtype != MSTF_OUT_F16) return MSTF_EINVAL;
+  if (!aligned16(o) || !aligned16(out) || (reinterpret_cast<uintptr_t>(ml) & 7u)) return MSTF_EINVAL;
+  if (head_dim != kD || group > kMaxGroup) return MSTF_ENOTSUP;
+  return launch_merge_partials(n, units, group, ml, o, out, out_dtype == MSTF_OUT_F16,
+                               static_cast<cudaStream_t>(stream)) == cudaSuccess ? MSTF_OK : MSTF_ECUDA;
+}
+
 int mstf_decode_step(mstf_cache* h, const void* k_new, const void* v_new, const void* q, float scale, void* out,
                      int32_t out_dtype, void* ws, size_t ws_bytes, void* stream) {
   if (!h || !k_new || !v_new || !aligned16(k_new) || !aligned16(v_new)) return MSTF_EINVAL;
@@ -307,6 +332,14 @@ int mstf_dense_decode_attention(const void* k, const void* v, const int32_t* len
                              group, t_max, dense_splits(units, t_max), static_cast<const uint16_t*>(q), scale, out,
                              out_dtype == MSTF_OUT_F16, ws, static_cast<cudaStream_t>(stream)) != cudaSuccess)
     return MSTF_ECUDA;
+  return MSTF_OK;
+}
+
+int mstf_seq_split(int32_t T, int32_t window, int32_t world, int32_t rank, int32_t* t0, int32_t* t1) {
+  if (T < 0 || window < 0 || world < 1 || rank < 0 || rank >= world || !t0 || !t1) return MSTF_EINVAL;
+  const int64_t C = T - (T < window ? T : window);  // prompt tokens that will be compressed
+  *t0 = (int32_t)(C * rank / world);
+  *t1 = rank == world - 1 ? T : (int32_t)(C * (rank + 1) / world);
   return MSTF_OK;
 }
 

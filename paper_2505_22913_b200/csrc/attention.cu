@@ -81,6 +81,8 @@ struct AttnParams {
   int* sk_pref;                     // stream-K ragged: per-unit item prefix in the workspace (U+1)
   void* out;
   int out_f16;
+  float* part_ml;  // non-null: write the softmax partials (m, l) [U][G][2] and o [U][G][kD] instead of O
+  float* part_o;
 };
 
 // ---------------------------------------------------------------- smem helpers
@@ -1560,8 +1562,13 @@ __global__ void __launch_bounds__(kMaxGroup * 32) mstf_sk_combine_kernel(const A
       acc.x += wi * v[i].x; acc.y += wi * v[i].y; acc.z += wi * v[i].z; acc.w += wi * v[i].w;
     }
   }
-  const float inv = 1.f / l_sum;
   const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
+  if (p.part_ml) {  // sequence-split shard: unnormalised partials (log2 domain)
+    *reinterpret_cast<float4*>(p.part_o + oi) = acc;
+    if (lane == 0) *reinterpret_cast<float2*>(p.part_ml + ((size_t)u * G + h) * 2) = make_float2(m_max, l_sum);
+    return;
+  }
+  const float inv = 1.f / l_sum;
   if (p.out_f16) {
     __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.out) + oi);
     po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
@@ -1574,7 +1581,7 @@ __global__ void __launch_bounds__(kMaxGroup * 32) mstf_sk_combine_kernel(const A
 
 // ---------------------------------------------------------------- K3: combine partials
 __global__ void mstf_combine_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml, int nparts,
-                                    int G, void* out, int out_f16) {
+                                    int G, void* out, int out_f16, float* part_ml, float* part_o) {
   pdl_launch_dependents();
   pdl_wait();  // partials come from the attention kernel just before
   // one warp per (unit, head); lane owns channels 4*lane .. 4*lane+3
@@ -1595,7 +1602,45 @@ __global__ void mstf_combine_kernel(const float* __restrict__ ws_o, const float*
     L += w * ml.y;
     acc.x += w * o.x; acc.y += w * o.y; acc.z += w * o.z; acc.w += w * o.w;
   }
+  const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
+  if (part_ml) {  // sequence-split shard: unnormalised partials (log2 domain)
+    *reinterpret_cast<float4*>(part_o + oi) = acc;
+    if (lane == 0) *reinterpret_cast<float2*>(part_ml + ((size_t)u * G + h) * 2) = make_float2(M, L);
+    return;
+  }
   const float inv = 1.f / L;
+  if (out_f16) {
+    __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(out) + oi);
+    po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
+    po[1] = __floats2half2_rn(acc.z * inv, acc.w * inv);
+  } else {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + oi) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  }
+}
+
+// Sequence-split merge (NEXT-3): n shards' partials [n][U][G] (m in log2 units, l, o unnormalised)
+// -> O = sum_i 2^(m_i - M) o_i / sum_i 2^(m_i - M) l_i, the a9 combine across shards. One warp per
+// (unit, head); an all-empty (unit, head) (L = 0) gives 0.
+__global__ void mstf_merge_kernel(int n, int U, int G, const float* __restrict__ ml, const float* __restrict__ o,
+                                  void* out, int out_f16) {
+  const int u = blockIdx.x, h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (h >= G) return;
+  float M = -INFINITY;
+  for (int i = lane; i < n; i += 32) M = fmaxf(M, ml[(((size_t)i * U + u) * G + h) * 2]);
+#pragma unroll
+  for (int s = 16; s; s >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, s));
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < n; ++i) {
+    const size_t pi = ((size_t)i * U + u) * G + h;
+    const float2 m = *reinterpret_cast<const float2*>(ml + pi * 2);
+    const float4 v = *(reinterpret_cast<const float4*>(o + pi * kD) + lane);
+    const float w = m.x == -INFINITY ? 0.f : exp2f(m.x - M);
+    L += w * m.y;
+    acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
   const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
   if (out_f16) {
     __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(out) + oi);
@@ -1605,6 +1650,13 @@ __global__ void mstf_combine_kernel(const float* __restrict__ ws_o, const float*
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + oi) =
         make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   }
+}
+
+cudaError_t launch_merge_partials(int32_t n, int32_t U, int32_t G, const float* ml, const float* o, void* out,
+                                  int32_t out_f16, cudaStream_t s) {
+  if (U == 0) return cudaSuccess;
+  mstf_merge_kernel<<<U, G * 32, 0, s>>>(n, U, G, ml, o, out, out_f16);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- dense baseline
@@ -1768,7 +1820,7 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
 
 cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, int32_t G, const uint16_t* q,
                                     float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s,
-                                    const FuseArgs* fuse) {
+                                    const FuseArgs* fuse, float* part_ml, float* part_o) {
   if (fuse && !plan.sk) return cudaErrorInvalidValue;  // the fused step needs the register kernel
   AttnParams p;
   p.c = c;
@@ -1793,6 +1845,8 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   p.ws_ml = p.ws_o + parts * G * kD;
   p.out = out;
   p.out_f16 = out_f16;
+  p.part_ml = part_ml;
+  p.part_o = part_o;
   p.sk = 0;
   p.sk_static = p.sk_nb = p.sk_c = p.sk_nchunks = p.sk_total = 0;
   p.sk_ctr = p.tickets + c.U;
@@ -1859,7 +1913,7 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
   e = launch_pdl(kern, dim3(plan.splits, c.U), dim3(kThreadsKV), (size_t)smem, s, p);
   if (e != cudaSuccess) return e;
   return launch_pdl(mstf_combine_kernel, dim3(c.U), dim3(G * 32), 0, s, (const float*)p.ws_o, (const float*)p.ws_ml,
-                    (int)(plan.splits * kConsumerWarps), (int)G, out, (int)out_f16);
+                    (int)(plan.splits * kConsumerWarps), (int)G, out, (int)out_f16, part_ml, part_o);
 }
 
 cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const int32_t* lengths, int32_t U,
@@ -1872,7 +1926,7 @@ cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const i
                                                                         scale * 1.4426950408889634f, ws_o, ws_ml);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  mstf_combine_kernel<<<U, G * 32, 0, s>>>(ws_o, ws_ml, splits * kConsumerWarps, G, out, out_f16);
+  mstf_combine_kernel<<<U, G * 32, 0, s>>>(ws_o, ws_ml, splits * kConsumerWarps, G, out, out_f16, nullptr, nullptr);
   return cudaGetLastError();
 }
 

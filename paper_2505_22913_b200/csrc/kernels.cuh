@@ -99,7 +99,11 @@ struct FuseArgs {
 };
 cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, int32_t G, const uint16_t* q,
                                     float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s,
-                                    const FuseArgs* fuse = nullptr);
+                                    const FuseArgs* fuse = nullptr, float* part_ml = nullptr,
+                                    float* part_o = nullptr);
+// Sequence split (NEXT-3): merge n shards' partials [n][U][G] into O [U][G][kD].
+cudaError_t launch_merge_partials(int32_t n, int32_t U, int32_t G, const float* ml, const float* o, void* out,
+                                  int32_t out_f16, cudaStream_t s);
 
 cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const int32_t* lengths, int32_t U,
                                    int32_t G, int32_t t_max, int32_t splits, const uint16_t* q, float scale,

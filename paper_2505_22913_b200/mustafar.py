@@ -30,6 +30,7 @@ EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "
            "mstf_dense_decode_attention", "mstf_shard_units", "mstf_decode_step",
            "mstf_decode_step_kernel_count", "mstf_attention_kernel_count",
            "mstf_set_key_weights", "mstf_query_abs_sum",
+           "mstf_seq_split", "mstf_sparse_decode_attention_partial", "mstf_merge_partials",
            "mstf_status_string", "mstf_build_info")
 
 
@@ -76,6 +77,9 @@ def lib() -> ctypes.CDLL:
         "mstf_attention_kernel_count": (ctypes.c_int, [vp]),
         "mstf_set_key_weights": (ctypes.c_int, [vp, vp]),
         "mstf_query_abs_sum": (ctypes.c_int, [vp, i32, i32, i32, i32, vp, vp]),
+        "mstf_seq_split": (ctypes.c_int, [i32, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "mstf_sparse_decode_attention_partial": (ctypes.c_int, [vp, vp, ctypes.c_float, vp, vp, vp, sz, vp]),
+        "mstf_merge_partials": (ctypes.c_int, [i32, i32, i32, i32, vp, vp, vp, i32, vp]),
         "mstf_status_string": (ctypes.c_char_p, [i32]),
         "mstf_build_info": (ctypes.c_char_p, []),
     }
@@ -127,6 +131,26 @@ def query_abs_sum(q: torch.Tensor, out: torch.Tensor | None = None, stream=None)
         out = torch.empty(U, d, dtype=torch.float32, device=q.device)
     _check("mstf_query_abs_sum", lib().mstf_query_abs_sum(_dev_ptr(q, name="q"), U, R, G, d,
                                                           _dev_ptr(out, torch.float32, "out"), _stream(stream)))
+    return out
+
+
+def seq_split(T: int, window: int, world: int, rank: int):
+    """Prompt token range [t0, t1) of `rank` in a sequence split (mstf_seq_split)."""
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _check("mstf_seq_split", lib().mstf_seq_split(T, window, world, rank, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def merge_partials(ml: torch.Tensor, o: torch.Tensor, out=None, out_dtype=torch.float32, stream=None):
+    """Merge shard partials ml float32 [n, U, G, 2], o float32 [n, U, G, d] -> out [U, G, d]
+    (mstf_merge_partials)."""
+    n, U, G, d = o.shape
+    if out is None:
+        out = torch.empty(U, G, d, dtype=out_dtype, device=o.device)
+    code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
+    _check("mstf_merge_partials", lib().mstf_merge_partials(n, U, G, d, _dev_ptr(ml, torch.float32, "ml"),
+                                                            _dev_ptr(o, torch.float32, "o"),
+                                                            _dev_ptr(out, out.dtype, "out"), code, _stream(stream)))
     return out
 
 
@@ -234,6 +258,23 @@ class MustafarCache:
         _check("mstf_prune_compress_kv",
                lib().mstf_prune_compress_kv(self._h, _dev_ptr(k, name="k"), _dev_ptr(v, name="v"), T, ln,
                                             _stream(stream)))
+
+    def sparse_decode_attention_partial(self, q: torch.Tensor, scale=None, ml=None, o=None, stream=None):
+        """Softmax partials of this cache's tokens (one shard of a sequence split):
+        ml float32 [U, G, 2] (m in log2 units, l), o float32 [U, G, d] unnormalised
+        (mstf_sparse_decode_attention_partial)."""
+        d, U, G = self.shape.head_dim, self.units, self.shape.group
+        scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+        if ml is None:
+            ml = torch.empty(U, G, 2, dtype=torch.float32, device=self.device)
+        if o is None:
+            o = torch.empty(U, G, d, dtype=torch.float32, device=self.device)
+        _check("mstf_sparse_decode_attention_partial",
+               lib().mstf_sparse_decode_attention_partial(self._h, _dev_ptr(q, name="q"), scale,
+                                                          _dev_ptr(ml, torch.float32, "ml"),
+                                                          _dev_ptr(o, torch.float32, "o"), self._ws.data_ptr(),
+                                                          self._ws.numel(), _stream(stream)))
+        return ml, o
 
     def set_key_weights(self, w: torch.Tensor | None):
         """Output-aware K pruning for later K compressions: w float32 [U, d] on the device

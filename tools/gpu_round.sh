@@ -14,4 +14,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-dense --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:mstf_attn -s 40 -c 1 \
    -o gpurun_out/prof_bench python bench.py --steps 2 --warmup 3 --no-dense --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+timeout 300 python tools/prefill_time.py > gpurun_out/prefill_time.txt 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_kernel -s 2 -c 1 \
+   -o gpurun_out/prof_prefill python tools/prefill_time.py 16 32 8 4096 39 > gpurun_out/ncu_prefill.log 2>&1
 ls -la gpurun_out
