@@ -40,6 +40,11 @@ __global__ void set_counters_uniform(int32_t* n_comp, int32_t* n_win, int U, int
 // gridDim.y); warp w of block x handles token groups of 4 starting at (8x + w) * 4 * kPrefillGroups.
 // Control flow is warp-uniform (a token past the row's end computes on zeros and stores nothing).
 constexpr int kPrefillGroups = 4;  // 4-token groups per warp
+#ifndef MSTF_PREFILL_HSET
+#define MSTF_PREFILL_HSET 1
+#endif
+__device__ __forceinline__ __half2 __ushort2_as_half2(uint32_t x) { return *reinterpret_cast<__half2*>(&x); }
+__device__ __forceinline__ uint32_t __half2_as_u32(__half2 x) { return *reinterpret_cast<uint32_t*>(&x); }
 __device__ __forceinline__ uint32_t shfl_down8(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d, 8); }
 __device__ __forceinline__ uint32_t shfl_up8(uint32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d, 8); }
 
@@ -114,6 +119,27 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
         t4 = cnt >= kk ? c4 : t4;
       }
       uint32_t t2 = (t4 & 0x7Fu) * 0x01000100u;  // tau, replicated in 2 halves
+#if MSTF_PREFILL_HSET
+      // bits 7..0 with fp16 compares: a magnitude is a non-negative fp16 value, and for those the
+      // order of the values is the order of the bit patterns (candidates >= 0x7C01 are NaNs and
+      // compare false, like every finite magnitude against them). __hge2 gives 1.0 / 0.0 per
+      // half; the sum starts at 1024.0, where the fp16 spacing is 1, so its bits are
+      // 0x6400 + count per half.
+      __half2 xm[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xm[i] = __ushort2_as_half2(w[i] & 0x7FFF7FFFu);
+#pragma unroll
+      for (int b = 7; b >= 0; --b) {
+        const uint32_t c2 = t2 | (0x00010001u << b);
+        const __half2 ch = __ushort2_as_half2(c2);
+        __half2 acc = __ushort2_as_half2(0x64006400u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc = __hadd2(acc, __hge2(xm[i], ch));
+        const uint32_t f = __half2_as_u32(acc) - 0x64006400u;  // half counts
+        const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x00010001u, 0, put2)), 0, take);
+        t2 = cnt >= kk ? c2 : t2;
+      }
+#else
 #pragma unroll
       for (int b = 7; b >= 0; --b) {
         const uint32_t c2 = t2 | (0x00010001u << b);
@@ -123,6 +149,7 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
         const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x00010001u, 0, put2)), 0, take);
         t2 = cnt >= kk ? c2 : t2;
       }
+#endif
       // keep mask of the lane's 16 channels: bit j <-> channel 16r + j (mag >= tau)
       uint32_t acc = 0;
 #pragma unroll
