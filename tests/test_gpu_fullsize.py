@@ -97,3 +97,66 @@ def test_fullsize_decode_step_sampled(M, name):
         o = out[u].cpu().numpy().astype(np.float64)
         err = float((np.abs(o - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max())
         assert err <= TOL, (name, u, err)
+
+
+def test_fullsize_output_aware_prefill_sampled(M):
+    """Output-aware K pruning (NEXT-2) at C2 size: weights from 32 window queries of the GQA
+    group (mstf_query_abs_sum), whole-cache prefill on the GPU, sampled units bit-exact
+    against the oracle's scored pruning."""
+    B, hq, hkv, T, sk, sv, sample = CASES["C2_b16_s70"]
+    U, G, d, W = B * hkv, hq // hkv, 128, 32
+    kk = O.keep_count(sk, d)
+    sK, sV, sQ = (synth.seed_for(9, i) for i in range(3))
+    K = synth.fp16_torch((U, T, d), sK, device="cuda", kind="outlier")
+    V = synth.fp16_torch((U, T, d), sV, device="cuda")
+    qr = synth.fp16_torch((U, 32, G, d), sQ, device="cuda")
+    w = M.query_abs_sum(qr)
+    gc = M.MustafarCache(B, hq, hkv, d, kk, kk, W, T)
+    gc.set_key_weights(w)
+    gc.prune_compress_kv(K, V)
+    del K, V
+    torch.cuda.synchronize()
+    bufs = gc.buffers()
+    wh = O.query_abs_sum(qr.cpu().view(torch.int16).numpy().view(np.uint16))
+    assert np.array_equal(w.cpu().numpy().view(np.uint32), wh.view(np.uint32))
+    for u in sample:
+        Ku = synth.fp16_np_rows((U, T, d), sK, u * T, T, kind="outlier").view(np.uint16)
+        Vu = synth.fp16_np_rows((U, T, d), sV, u * T, T).view(np.uint16)
+        oc = O.OracleCache(1, d, kk, kk, W, T)
+        oc.set_key_weights(wh[u][None])
+        oc.prefill(Ku[None], Vu[None])
+        nc = int(oc.n_comp[0])
+        assert np.array_equal(bufs["bitmap_k"][u, :nc].cpu().numpy().view(np.uint64), oc.bitmap_k[0, :nc])
+        assert np.array_equal(bufs["values_k"][u, :nc].cpu().numpy().view(np.uint16), oc.values_k[0, :nc])
+        assert np.array_equal(bufs["bitmap_v"][u, :nc].cpu().numpy().view(np.uint64), oc.bitmap_v[0, :nc])
+
+
+def test_fullsize_sequence_split_sampled(M):
+    """Sequence split (NEXT-3) at the batch-1 128K shape: 4 shards on one device, partials
+    merged, sampled units against the oracle over the unsplit cache."""
+    B, hq, hkv, T, world = 1, 32, 8, 131072, 4
+    U, G, d, W = B * hkv, hq // hkv, 128, 32
+    kk = O.keep_count(0.7, d)
+    sK, sV, sQ = (synth.seed_for(10, i) for i in range(3))
+    K = synth.fp16_torch((U, T, d), sK, device="cuda")
+    V = synth.fp16_torch((U, T, d), sV, device="cuda")
+    q = synth.fp16_torch((U, G, d), sQ, device="cuda")
+    ml = torch.empty(world, U, G, 2, dtype=torch.float32, device="cuda")
+    po = torch.empty(world, U, G, d, dtype=torch.float32, device="cuda")
+    for r in range(world):
+        t0, t1 = M.seq_split(T, W, world, r)
+        c = M.MustafarCache(B, hq, hkv, d, kk, kk, W if r == world - 1 else 0, t1 - t0)
+        c.prune_compress_kv(K[:, t0:t1].contiguous(), V[:, t0:t1].contiguous())
+        c.sparse_decode_attention_partial(q, 1 / math.sqrt(d), ml=ml[r], o=po[r])
+        del c
+    del K, V
+    out = M.merge_partials(ml, po).cpu().numpy().astype(np.float64)
+    qh = q.cpu().view(torch.int16).numpy().view(np.uint16)
+    for u in (0, 5):
+        Ku = synth.fp16_np_rows((U, T, d), sK, u * T, T).view(np.uint16)
+        Vu = synth.fp16_np_rows((U, T, d), sV, u * T, T).view(np.uint16)
+        oc = O.OracleCache(1, d, kk, kk, W, T)
+        oc.prefill(Ku[None], Vu[None])
+        ref = O.attention(oc, qh[u][None], 1 / math.sqrt(d))[0]
+        err = float((np.abs(out[u] - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max())
+        assert err <= TOL, (u, err)
