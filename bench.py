@@ -223,6 +223,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         return q, kn, vn
 
     outs = [torch.empty(U, G, d, dtype=torch.float16, device=dev) for _ in range(L)]
+    # --gather: every layer's output is all-gathered in place into the
+    # [B_global][Hq][d] tensor (rank r's slice is its units' [U][G][d]) -- the serving layout.
+    # Off by default: the units are independent, so the measured path has no collective.
+    gather = args.gather and world > 1
+    full = [torch.empty(world * U, G, d, dtype=torch.float16, device=dev) for _ in range(L)] if gather else None
+    if gather:
+        outs = [f[rank * U:(rank + 1) * U] for f in full]
     torch.cuda.synchronize()
 
     def step(slab, ev=None):
@@ -235,6 +242,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             caches[l].decode_step(kn, vn, q, scale, out=outs[l])
             if ev is not None:
                 ev[l][1].record()
+            if gather:
+                dist.all_gather_into_tensor(full[l], outs[l])  # in place: outs[l] is this rank's slice
 
     # ---- device-timed region
     sampler = ClockSampler(local_rank)
@@ -384,7 +393,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded splitmix64 -> fp16 ~N(0,1)); no model weights",
         "config": {"workload": args.workload, "desc": cfg["desc"], "batch_per_gpu": B, "global_batch": B * world,
                    "num_q_heads": hq, "num_kv_heads": hkv, "head_dim": d, "context": T, "keep_k": kk, "keep_v": kv,
-                   "window": W_WINDOW, "layers": L, "parallelism": f"dp{world} (batch x kv-head units, no collective)",
+                   "window": W_WINDOW, "layers": L, "parallelism": f"dp{world} (batch x kv-head units, " + ("in-place all_gather of every layer's output)" if gather else "no collective)"),
                    "l2": f"inputs larger than L2: {L} layer caches x {caches[0].nbytes / 1e6:.0f} MB"},
         "us_per_layer_step": round(ms * 1e3 / L, 3),
         "decode_step_us_per_call_events": round(attn_us, 3),  # second pass: events around each call
@@ -447,6 +456,8 @@ def main():
     ap.add_argument("--workload", default="C2", choices=list(WORKLOADS))
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--no-dense", dest="dense", action="store_false")
+    ap.add_argument("--gather", action="store_true",
+                    help="N>1: all-gather every layer's output into [B][Hq][d] (a10; off by default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
