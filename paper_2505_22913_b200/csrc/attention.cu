@@ -995,21 +995,32 @@ __device__ __forceinline__ void load_raw(RawRegs<NCH>& rr, const uint16_t* __res
   rr.bm1 = g + 8 < nvalid ? ld(bw + (size_t)(tok0 + g + 8) * 4 + t) : 0u;
 }
 
+// Absolute shared address of this lane's first pair-array entry (row m0 of its token's column):
+// a function of the lane only, computed once per warp (outside the block loop). The V region
+// base is picked with selects, not a switch (a runtime switch on a lane-dependent index makes
+// the warp diverge).
 template <int NCH, bool IS_V>
-__device__ __forceinline__ void store_pairs(uint8_t* smem, const RawRegs<NCH>& rr, uint32_t ybase, int lane) {
+__device__ __forceinline__ uint32_t pair_dst(const uint8_t* smem, uint32_t ybase, int lane) {
   using Gm = PairGeom<NCH>;
   const int tau = lane >> 1, h = lane & 1;
   const int m0 = h ? Gm::kp / 2 + 2 : 0;
-  uint32_t dst, step;
+  uint32_t dst;
   if (IS_V) {
     const int r = (tau & 1) + 2 * (tau >> 3);
-    dst = ybase + 4u * (uint32_t)(VLayout<NCH>::region(r) + ((tau >> 1) & 3) + 4 * m0);
-    step = 16;
+    using VL = VLayout<NCH>;
+    const int reg = r == 0 ? VL::v0 : r == 1 ? VL::v1 : r == 2 ? VL::v2 : VL::v3;
+    dst = ybase + 4u * (uint32_t)(reg + ((tau >> 1) & 3) + 4 * m0);
   } else {
     dst = ybase + 4u * (uint32_t)((tau >> 3 ? KLayout<NCH>::k1 : KLayout<NCH>::k0) + (tau & 7) + 8 * m0);
-    step = 32;
   }
-  const uint32_t adst = opaque(dst + smem_u32(smem));
+  return dst + smem_u32(smem);
+}
+
+template <int NCH, bool IS_V>
+__device__ __forceinline__ void store_pairs(uint32_t adst_in, const RawRegs<NCH>& rr) {
+  using Gm = PairGeom<NCH>;
+  constexpr uint32_t step = IS_V ? 16 : 32;
+  const uint32_t adst = opaque(adst_in);
 #pragma unroll
   for (int e = 0; e < Gm::E; ++e) {
     const uint32_t y = (e & 1) ? rr.W[(e + 1) >> 1] : prmt(rr.W[e >> 1], rr.W[(e >> 1) + 1], 0x5432);
@@ -1304,13 +1315,14 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         // once a block's words are in the pair array its registers are dead, so the next
         // block's loads go into them right away and overlap the gathers, MMAs and softmax.
         RawRegs<NK> rr;
+        const uint32_t pdst = pair_dst<NK, false>(smem, ybase, lane);
         int b = bbeg;
         if (b < bend) load(rr, b);
 #pragma unroll 1
         for (; b < bend; ++b) {
           const int nvalid = min(16, n - b * 16);
           __syncwarp();
-          store_pairs<NK, false>(smem, rr, ybase, lane);
+          store_pairs<NK, false>(pdst, rr);
           const uint32_t bm0 = rr.bm0, bm1 = rr.bm1;
           if (b + 1 < bend) load(rr, b + 1);
           const uint32_t pk = __popc(bm0) | (__popc(bm1) << 16);
@@ -1440,12 +1452,13 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
         // one raw buffer: refilled with the next block as soon as this block's pair array and
         // bitmap words are extracted (see the K-warp loop)
         RawRegs<NV> rr;
+        const uint32_t pdst = pair_dst<NV, true>(smem, ybase, lane);
         int b = bbeg;
         if (b < bend) load(rr, b);
 #pragma unroll 1
         for (; b < bend; ++b) {
           __syncwarp();
-          store_pairs<NV, true>(smem, rr, ybase, lane);
+          store_pairs<NV, true>(pdst, rr);
           const uint32_t pv = __popc(rr.bm0) | (__popc(rr.bm1) << 16);
           uint32_t iv = pv;
 #pragma unroll
