@@ -1304,11 +1304,14 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
       };
       {
         // unit base pointers are re-derived per load (sg[0], params) to save registers
+        const size_t ub = (size_t)u * c.cap;
+        const uint16_t* const vbase = c.val[0] + ub * c.kpad[0];
+        const uint64_t* const bbase = c.bm[0] + ub * kTiles;
+        const int wait_blk = (p.fuse && p.evict) ? nbc - 1 : -1;
         auto load = [&](RawRegs<NK>& rr, int bb) {
-          const size_t ub = (size_t)sg[0] * c.cap;
           // the last block holds the record the fused append wrote: wait for its flag
-          if (p.fuse && p.evict && bb == nbc - 1) wait_ready(p.ready + u, p.epoch, lane);
-          load_raw<NK>(rr, c.val[0] + ub * c.kpad[0], c.bm[0] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
+          if (bb == wait_blk) wait_ready(p.ready + u, p.epoch, lane);
+          load_raw<NK>(rr, vbase, bbase, bb * 16, min(16, n - bb * 16), lane);
         };
         // One loop body (not a two-way unrolled ping-pong): the kernel's code footprint is what
         // the instruction cache sees with K- and V-warps resident together. One raw buffer:
@@ -1443,11 +1446,14 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
       };
       {
         // unit base pointers are re-derived per load (saves registers in the hot loop)
+        const size_t ub = (size_t)u * c.cap;
+        const uint16_t* const vbase = c.val[1] + ub * c.kpad[1];
+        const uint64_t* const bbase = c.bm[1] + ub * kTiles;
+        const int wait_blk = (p.fuse && p.evict) ? nbc - 1 : -1;
         auto load = [&](RawRegs<NV>& rr, int bb) {
-          const size_t ub = (size_t)u * c.cap;
           // the last block holds the record the fused append wrote: wait for its flag
-          if (p.fuse && p.evict && bb == nbc - 1) wait_ready(p.ready + c.U + u, p.epoch, lane);
-          load_raw<NV>(rr, c.val[1] + ub * c.kpad[1], c.bm[1] + ub * kTiles, bb * 16, min(16, n - bb * 16), lane);
+          if (bb == wait_blk) wait_ready(p.ready + c.U + u, p.epoch, lane);
+          load_raw<NV>(rr, vbase, bbase, bb * 16, min(16, n - bb * 16), lane);
         };
         // one raw buffer: refilled with the next block as soon as this block's pair array and
         // bitmap words are extracted (see the K-warp loop)
