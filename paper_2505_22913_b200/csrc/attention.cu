@@ -403,14 +403,18 @@ __device__ __forceinline__ void gather8_s(const uint8_t* smem, uint32_t hw, uint
 // entry (kept values before word wv).
 template <int STRIDE>
 __device__ __forceinline__ void gather8_il(uint32_t wv, uint32_t base, int h, uint32_t (&out)[8]) {
-  // bits p = 4i + 2h, p + 1 sit in byte i/2 at bit 4(i&1) + 2h
-  const uint32_t ce0 = wv << (7 - 2 * h), ce1 = wv << (6 - 2 * h);  // i even
-  const uint32_t co0 = wv << (3 - 2 * h), co1 = wv << (2 - 2 * h);  // i odd
+  // bits p = 4i + 2h, p + 1 sit in byte i/2 at bit 4(i&1) + 2h. One lane-dependent shift
+  // (wp = wv << (2 - 2h)); every other shift is by an immediate, so it can issue on the FMA pipe
+  // (IMAD.SHL) instead of the busier ALU pipe. Dropping wv's top bits for h = 0 is harmless: no
+  // shift below needs bits above 28 + 2h.
+  const uint32_t wp = wv << (2 - 2 * h);
+  const uint32_t ce0 = wp * (1u << 5), ce1 = wp * (1u << 4);  // i even: wv << (7 - 2h), << (6 - 2h)
+  const uint32_t co0 = wp * 2u, co1 = wp;                      // i odd:  wv << (3 - 2h), << (2 - 2h)
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t m = i >> 1;
     const uint32_t sel = (8u | m) | ((8u | m) << 4) | ((12u | m) << 8) | ((12u | m) << 12);
-    const uint32_t pc = __popc(wv << (31 - 4 * i - 2 * h));  // kept channels <= 4i + 2h
+    const uint32_t pc = __popc(wp * (1u << (29 - 4 * i)));  // kept channels <= 4i + 2h
     out[i] = lds_abs_masked(base + STRIDE * pc, (i & 1) ? prmt(co0, co1, sel) : prmt(ce0, ce1, sel));
   }
 }
