@@ -85,6 +85,15 @@ struct AttnParams {
   float* part_o;
 };
 
+// 2^x with the single MUFU.EX2 (ex2.approx.ftz): the arguments are s - max <= 0, results in
+// (0, 1]; results below 2^-126 flush to 0 (weights that small do not change an fp32 sum of
+// terms >= 1). exp2f adds a range check and two multiplies per call for subnormal results.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ---------------------------------------------------------------- smem helpers
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
@@ -551,8 +560,8 @@ __device__ __forceinline__ void process_block(const BlockRegs& r, bool vg, bool 
     bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
   }
   const float mn0 = fmaxf(st.m0, bm0), mn1 = fmaxf(st.m1, bm1);
-  const float a0 = exp2f(st.m0 - mn0), a1 = exp2f(st.m1 - mn1);
-  const float p0 = exp2f(x0 - mn0), p1 = exp2f(x1 - mn1), p2 = exp2f(x2 - mn0), p3 = exp2f(x3 - mn1);
+  const float a0 = fast_exp2(st.m0 - mn0), a1 = fast_exp2(st.m1 - mn1);
+  const float p0 = fast_exp2(x0 - mn0), p1 = fast_exp2(x1 - mn1), p2 = fast_exp2(x2 - mn0), p3 = fast_exp2(x3 - mn1);
   st.l0 = st.l0 * a0 + (p0 + p2);
   st.l1 = st.l1 * a1 + (p1 + p3);
   st.m0 = mn0;
@@ -606,8 +615,8 @@ __device__ __forceinline__ uint4 k_block(const uint32_t (&kr)[2][16], bool vg, b
     bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
   }
   const float mn0 = fmaxf(st.m0, bm0), mn1 = fmaxf(st.m1, bm1);
-  const float a0 = exp2f(st.m0 - mn0), a1 = exp2f(st.m1 - mn1);
-  const float p0 = exp2f(x0 - mn0), p1 = exp2f(x1 - mn1), p2 = exp2f(x2 - mn0), p3 = exp2f(x3 - mn1);
+  const float a0 = fast_exp2(st.m0 - mn0), a1 = fast_exp2(st.m1 - mn1);
+  const float p0 = fast_exp2(x0 - mn0), p1 = fast_exp2(x1 - mn1), p2 = fast_exp2(x2 - mn0), p3 = fast_exp2(x3 - mn1);
   st.l0 = st.l0 * a0 + (p0 + p2);
   st.l1 = st.l1 * a1 + (p1 + p3);
   st.m0 = mn0;
