@@ -208,6 +208,8 @@ int mstf_seq_split(int32_t T, int32_t window, int32_t world, int32_t rank, int32
  *   ml [U][G][2]: m = max_t s_t*log2(e), l = sum_t 2^(s_t*log2(e) - m);  o [U][G][d]:
  *   o = sum_t 2^(s_t*log2(e) - m) * v_t (not divided by l), s_t = scale * q . k_t.
  * q, scale, workspace as in mstf_sparse_decode_attention. ml 8-byte aligned, o 16-byte aligned.
+ * A cache in which EVERY unit is empty (a rank that holds no token, e.g. T < world) writes the
+ * merge identity m = -inf, l = 0, o = 0; some-but-not-all units empty is EEMPTY.
  * Errors: as mstf_sparse_decode_attention.                                                     */
 int mstf_sparse_decode_attention_partial(const mstf_cache* cache, const void* q, float scale, float* ml,
                                          float* o, void* workspace, size_t workspace_bytes, void* stream);

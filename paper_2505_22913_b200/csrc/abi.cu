@@ -234,10 +234,15 @@ int mstf_sparse_decode_attention_partial(const mstf_cache* h, const void* q, flo
   const int st = check_attention_args(h, q, ml, MSTF_OUT_F32, ws, ws_bytes);
   if (st != MSTF_OK) return st;
   if (!o || !aligned16(o) || (reinterpret_cast<uintptr_t>(ml) & 7u)) return MSTF_EINVAL;
+  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
+  bool all_empty = true;
+  for (int32_t u = 0; u < h->view.U; ++u) all_empty = all_empty && h->nc[u] + h->nw[u] == 0;
+  if (all_empty)  // a shard that holds no token of the sequence (e.g. T < world): the merge identity
+    return launch_empty_partials(ml, o, h->view.U * G, static_cast<cudaStream_t>(stream)) == cudaSuccess
+               ? MSTF_OK : MSTF_ECUDA;
   AttnPlan plan;
   const int sp = make_plan(h, h->nc, h->nw, &plan);
   if (sp != MSTF_OK) return sp;
-  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
   if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, nullptr, 0, ws,
                               static_cast<cudaStream_t>(stream), nullptr, ml, o) != cudaSuccess)
     return MSTF_ECUDA;

@@ -1684,6 +1684,23 @@ __global__ void mstf_merge_kernel(int n, int U, int G, const float* __restrict__
   }
 }
 
+// The partials of a shard without tokens: m = -inf, l = 0, o = 0 (the merge's identity).
+__global__ void mstf_empty_partial_kernel(float* __restrict__ ml, float* __restrict__ o, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    reinterpret_cast<float2*>(ml)[i] = make_float2(-INFINITY, 0.f);
+    float4* po = reinterpret_cast<float4*>(o + (size_t)i * kD);
+#pragma unroll
+    for (int j = 0; j < kD / 4; ++j) po[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+cudaError_t launch_empty_partials(float* ml, float* o, int32_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  mstf_empty_partial_kernel<<<(n + 127) / 128, 128, 0, s>>>(ml, o, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge_partials(int32_t n, int32_t U, int32_t G, const float* ml, const float* o, void* out,
                                   int32_t out_f16, cudaStream_t s) {
   if (U == 0) return cudaSuccess;

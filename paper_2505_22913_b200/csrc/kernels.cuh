@@ -101,6 +101,8 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
                                     float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s,
                                     const FuseArgs* fuse = nullptr, float* part_ml = nullptr,
                                     float* part_o = nullptr);
+// Sequence split (NEXT-3): partials of an empty shard (m = -inf, l = 0, o = 0), n = U * G.
+cudaError_t launch_empty_partials(float* ml, float* o, int32_t n, cudaStream_t s);
 // Sequence split (NEXT-3): merge n shards' partials [n][U][G] into O [U][G][kD].
 cudaError_t launch_merge_partials(int32_t n, int32_t U, int32_t G, const float* ml, const float* o, void* out,
                                   int32_t out_f16, cudaStream_t s);

@@ -89,3 +89,25 @@ def test_merge_empty_and_f16(M):
     torch.cuda.synchronize()
     assert torch.allclose(out[0].float(), (o[1, 0] / 2.0), rtol=2e-3, atol=1e-3)
     assert torch.count_nonzero(out[1]) == 0
+
+
+def test_seq_split_more_ranks_than_compressed_tokens(M):
+    """T <= W: every compressed range is empty; those shards return the merge identity and
+    the merge equals the unsplit attention (all tokens in the last shard's window)."""
+    B_, hq, hkv, T, W, world = 1, 8, 2, 20, 32, 4
+    U, G = B_ * hkv, hq // hkv
+    K = synth.fp16_np((U, T, 128), 91)
+    V = synth.fp16_np((U, T, 128), 92)
+    q = synth.fp16_np((U, G, 128), 93)
+    ml = torch.empty(world, U, G, 2, dtype=torch.float32, device="cuda")
+    o = torch.empty(world, U, G, 128, dtype=torch.float32, device="cuda")
+    for r in range(world):
+        t0, t1 = M.seq_split(T, W, world, r)
+        c = M.MustafarCache(B_, hq, hkv, 128, 39, 39, W if r == world - 1 else 0, max(t1 - t0, 1))
+        if t1 > t0:
+            c.prune_compress_kv(dev(K[:, t0:t1]), dev(V[:, t0:t1]))
+        c.sparse_decode_attention_partial(dev(q), 0.1, ml=ml[r], o=o[r])
+    out = M.merge_partials(ml, o).cpu().numpy()
+    oc = O.OracleCache(U, 128, 39, 39, W, T)
+    oc.prefill(K.view(np.uint16), V.view(np.uint16))
+    assert rel_err(out, O.attention(oc, q.view(np.uint16), 0.1)) <= 2e-3
