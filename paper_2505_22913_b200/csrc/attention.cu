@@ -1840,7 +1840,11 @@ AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_
     int64_t grid = 2 * (int64_t)sm_count;
     if (const char* e = std::getenv("MSTF_SKGRID")) grid = std::atoi(e);  // dev: occupancy scan
     if (grid > kMaxSkGrid) grid = kMaxSkGrid;
-    const int64_t min_q = 8;  // >= 2 items per worker to amortise the segment prologue
+    // >= 14 cost units per CTA (3.5 per worker) to amortise each worker's segment prologue and
+    // keep the combine's partials per unit few: at batch 1 (C2 shape, 8 units) this picks 148
+    // CTAs instead of 260, 22.6 -> 19.3 us per step (tools/grid_scan.py); from batch 2 up the
+    // grid stays at 2 CTAs per SM
+    const int64_t min_q = 14;
     if (grid > (total_items + min_q - 1) / min_q) grid = (total_items + min_q - 1) / min_q;
     if (grid < 1) grid = 1;
     const int64_t np = 4 * grid;
