@@ -1552,22 +1552,31 @@ __global__ void __launch_bounds__(256, 2) mstf_attn_reg_kernel(const AttnParams 
 // (unit_parts). Phase 1: lanes load (m, l) of different slots in parallel and reduce the max
 // with shuffles; phase 2: a branch-free loop accumulates w_i * o_i (weights broadcast from
 // the lane that holds them), so the slot loads of successive iterations overlap.
-__global__ void __launch_bounds__(kMaxGroup * 32) mstf_sk_combine_kernel(const AttnParams p) {
+// S = blockDim.x / (32 G) sub-warps per head split the unit's slots (S > 1 when a unit has many
+// slots, i.e. few units: at batch 1 a unit holds ~70 partials); sub-warp results meet in shared
+// memory and sub-warp 0 finishes.
+constexpr int kCombineMaxSub = 4;
+constexpr int kCombineMaxThreads = 512;  // keeps 128 registers per thread (the 16-slot batch)
+template <bool SUB>  // false: one warp per head (S = 1, the many-unit case), exactly the plain loop
+__global__ void __launch_bounds__(SUB ? kCombineMaxThreads : kMaxGroup * 32) mstf_sk_combine_kernel(const AttnParams p) {
   pdl_launch_dependents();
   pdl_wait();  // partials come from the attention kernel just before
-  const int u = blockIdx.x, h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  extern __shared__ __align__(16) float s_comb[];  // (S - 1) x G x kD accumulators, then (S - 1) x G (m, l)
   const int G = p.G;
-  if (h >= G) return;
+  const int u = blockIdx.x, wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = SUB ? wi % G : wi, sub = SUB ? wi / G : 0, S = SUB ? blockDim.x / (32 * G) : 1;
+  if (!SUB && h >= G) return;
   const int us = p.sk_nb ? u * p.sk_nb : p.sk_pref[u];
   const int ue = p.sk_nb ? (u + 1) * p.sk_nb : p.sk_pref[u + 1];
   const PartRanges r = unit_parts(p, u, us, ue);
   const int np = r.n1 + r.n2;
+  const int i_lo = np * sub / S, i_hi = np * (sub + 1) / S;
   auto slot = [&](int i) -> size_t { return i < r.n1 ? (size_t)(r.b1 + i) : (size_t)(r.b2 + i - r.n1); };
   float m_max = -INFINITY, l_sum = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   constexpr int kB = 16;  // slots per batch: all their loads are issued before any math
-  for (int i0 = 0; i0 < np; i0 += kB) {
-    const int cnt = min(kB, np - i0);
+  for (int i0 = i_lo; i0 < i_hi; i0 += kB) {
+    const int cnt = min(kB, i_hi - i0);
     float2 ml = make_float2(-INFINITY, 0.f);
     if (lane < cnt) ml = *reinterpret_cast<const float2*>(p.ws_ml + (slot(i0 + lane) * G + h) * 2);
     float4 v[kB];
@@ -1590,8 +1599,29 @@ __global__ void __launch_bounds__(kMaxGroup * 32) mstf_sk_combine_kernel(const A
     m_max = mn;
 #pragma unroll
     for (int i = 0; i < kB; ++i) {
-      const float wi = __shfl_sync(0xffffffffu, wgt, i);
-      acc.x += wi * v[i].x; acc.y += wi * v[i].y; acc.z += wi * v[i].z; acc.w += wi * v[i].w;
+      const float wi2 = __shfl_sync(0xffffffffu, wgt, i);
+      acc.x += wi2 * v[i].x; acc.y += wi2 * v[i].y; acc.z += wi2 * v[i].z; acc.w += wi2 * v[i].w;
+    }
+  }
+  if (SUB && S > 1) {
+    float* s_acc = s_comb;                                              // [S-1][G][kD]
+    float2* s_ml = reinterpret_cast<float2*>(s_comb + (S - 1) * G * kD);  // [S-1][G]
+    if (sub > 0) {
+      *reinterpret_cast<float4*>(s_acc + ((sub - 1) * G + h) * kD + 4 * lane) = acc;
+      if (lane == 0) s_ml[(sub - 1) * G + h] = make_float2(m_max, l_sum);
+    }
+    __syncthreads();
+    if (sub > 0) return;
+    for (int j = 0; j < S - 1; ++j) {
+      const float2 o = s_ml[j * G + h];
+      const float mn = fmaxf(m_max, o.x);
+      if (mn == -INFINITY) continue;
+      const float a = exp2f(m_max - mn), b2 = exp2f(o.x - mn);
+      const float4 x = *reinterpret_cast<const float4*>(s_acc + (j * G + h) * kD + 4 * lane);
+      acc.x = acc.x * a + x.x * b2; acc.y = acc.y * a + x.y * b2;
+      acc.z = acc.z * a + x.z * b2; acc.w = acc.w * a + x.w * b2;
+      l_sum = l_sum * a + o.y * b2;
+      m_max = mn;
     }
   }
   const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
@@ -1959,7 +1989,14 @@ cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, in
     if (e != cudaSuccess) return e;
     e = launch_pdl(rk, grid, dim3(256), (size_t)rsmem, s, pr);
     if (e != cudaSuccess) return e;
-    return launch_pdl(mstf_sk_combine_kernel, dim3(c.U), dim3(32 * G), 0, s, pr);
+    // sub-warps per head: ~16 partial slots each (one load batch), at most kCombineMaxSub
+    const int64_t slots_per_unit = (4 * (int64_t)plan.sk_grid + c.U - 1) / c.U + 2;
+    int sub = (int)((slots_per_unit + 15) / 16);
+    if (const char* e = std::getenv("MSTF_COMBSUB")) sub = std::atoi(e);  // dev A/B
+    sub = std::max(1, std::min(std::min(sub, kCombineMaxSub), kCombineMaxThreads / (32 * G)));
+    const size_t csmem = (size_t)(sub - 1) * G * (kD * sizeof(float) + sizeof(float2));
+    if (sub == 1) return launch_pdl(mstf_sk_combine_kernel<false>, dim3(c.U), dim3(32 * G), 0, s, pr);
+    return launch_pdl(mstf_sk_combine_kernel<true>, dim3(c.U), dim3(32 * G * sub), csmem, s, pr);
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
