@@ -36,6 +36,8 @@ W_WINDOW = 32
 WORKLOADS = {
     "C2": dict(desc="Llama-3-8B shape decode, 32 q / 8 kv heads, d=128, 4K context, batch 16, K/V 70% sparsity",
                batch=16, hq=32, hkv=8, T=4096, sk=0.7, sv=0.7),
+    "C2_b1": dict(desc="Llama-3-8B shape decode, 4K context, batch 1, K/V 70% sparsity",
+                  batch=1, hq=32, hkv=8, T=4096, sk=0.7, sv=0.7),
     "C2_s50": dict(desc="Llama-3-8B shape decode, 4K context, batch 16, K/V 50% sparsity",
                    batch=16, hq=32, hkv=8, T=4096, sk=0.5, sv=0.5),
     "C3": dict(desc="Llama-2-7B shape MHA decode, 32 heads, d=128, 32K context, batch 1, 70% sparsity",
@@ -299,20 +301,31 @@ def run_ours(args, cfg, rank, world, local_rank):
         outs = [f[rank * U:(rank + 1) * U] for f in full]
     torch.cuda.synchronize()
 
+    # per-(slab, layer) input views built once, outside the timed region: at small batch the
+    # step is short enough for per-call Python slicing to starve the GPU
+    view_cache = {}
+    cur_stream = torch.cuda.current_stream()
+
     def step(slab, ev=None):
         # one decode step per layer: append (a4) + attention (Alg. 1) in one C-ABI call
         # (mstf_decode_step: a single fused launch + the split combine for uniform caches)
+        key = slab.data_ptr()
+        vs = view_cache.get(key)
+        if vs is None:
+            vs = view_cache[key] = [views(slab, l) for l in range(L)]
         for l in range(L):
-            q, kn, vn = views(slab, l)
+            q, kn, vn = vs[l]
             if ev is not None:
                 ev[l][0].record()
-            caches[l].decode_step(kn, vn, q, scale, out=outs[l])
+            caches[l].decode_step(kn, vn, q, scale, out=outs[l], stream=cur_stream)
             if ev is not None:
                 ev[l][1].record()
             if gather:
                 dist.all_gather_into_tensor(full[l], outs[l])  # in place: outs[l] is this rank's slice
 
     # ---- device-timed region
+    for s_ in range(total_steps):
+        view_cache[gen[s_].data_ptr()] = [views(gen[s_], l) for l in range(L)]
     sampler = ClockSampler(local_rank)
     attn_ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(L)] for _ in range(K_steps)]
     for s in range(W_steps):
@@ -352,6 +365,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     host_in.copy_(gen[W_steps:W_steps + e2e_steps].cpu())  # same inputs as the headline pass
     host_out = torch.empty((e2e_steps, U, G, d), dtype=torch.float16, pin_memory=True)
     dev_in = [torch.empty((L, per_layer), dtype=torch.float16, device=dev) for _ in range(2)]
+    for b_ in dev_in:
+        view_cache[b_.data_ptr()] = [views(b_, l) for l in range(L)]
     copy_stream = torch.cuda.Stream(device=dev)
     compute = torch.cuda.current_stream()
     ready = [torch.cuda.Event() for _ in range(2)]      # inputs of buffer b are on the device
