@@ -113,6 +113,18 @@ def test_host_validation_before_launch(L):
         assert L.mstf_query_abs_sum(None, 4, 32, 4, 128, ctypes.c_void_p(0x1000), None) == -1
         assert L.mstf_query_abs_sum(ctypes.c_void_p(0x1000), 4, 32, 0, 128, ctypes.c_void_p(0x1000), None) == -1
         assert L.mstf_query_abs_sum(ctypes.c_void_p(0x1000), -1, 32, 4, 128, ctypes.c_void_p(0x1000), None) == -1
+        # sequence split: partials need a 16-B aligned o and 8-B aligned ml; merge argument checks
+        a = ctypes.c_void_p(0x4000)
+        assert L.mstf_sparse_decode_attention_partial(h, q, 0.1, a, None, ctypes.c_void_p(0x3000), ws, None) == -1
+        assert L.mstf_sparse_decode_attention_partial(h, q, 0.1, ctypes.c_void_p(0x4004), a,
+                                                      ctypes.c_void_p(0x3000), ws, None) == -1
+        assert L.mstf_merge_partials(0, 4, 4, 128, a, a, a, 0, None) == -1
+        assert L.mstf_merge_partials(2, 4, 4, 128, a, a, a, 5, None) == -1
+        assert L.mstf_merge_partials(2, 4, 4, 64, a, a, a, 0, None) == -7
+        assert L.mstf_merge_partials(2, 4, 16, 128, a, a, a, 0, None) == -7
+        t0, t1 = ctypes.c_int32(), ctypes.c_int32()
+        assert L.mstf_seq_split(100, 32, 4, 4, ctypes.byref(t0), ctypes.byref(t1)) == -1
+        assert L.mstf_seq_split(100, 32, 4, 3, ctypes.byref(t0), ctypes.byref(t1)) == 0 and t1.value == 100
     finally:
         L.mstf_cache_destroy(h)
 
