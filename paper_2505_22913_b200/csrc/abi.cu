@@ -392,8 +392,8 @@ int mstf_attention_kernel_count(const mstf_cache* h) {
   return 2;
 }
 
-// Dev tooling, not declared in include/mustafar.h: per-CTA {start ns, end ns, smid} of the last
-// attention launch made with MSTF_TRACE set.
+// Dev tooling (declared in include/mustafar.h, "Development only"): the per-CTA timeline of the
+// last attention launch made with MSTF_TRACE set.
 int mstf_dev_trace(void* host, int32_t n) { return copy_trace(host, n) == cudaSuccess ? MSTF_OK : MSTF_ECUDA; }
 
 const char* mstf_build_info(void) { return "mustafar-b200 sm_100a (mma.sync m16n8k16, cp.async.bulk, mbarrier)"; }
