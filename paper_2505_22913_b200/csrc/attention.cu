@@ -213,49 +213,6 @@ __device__ __forceinline__ void gather_half8(const uint8_t* smem, uint32_t hw, u
 #undef MSTF_G
 }
 
-template <int NK, int NV>
-__device__ __forceinline__ void fill_compressed(const CompBlock& cb, uint8_t* smem, BlockRegs& r, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-  // pair arrays for K and V of the warp's 16 tokens
-  build_pairs<NK>(smem, cb.kval, cb.yk, cb.kpk, cb.strk, cb.tok0, lane);
-  build_pairs<NV>(smem, cb.vval, cb.yv, cb.kpv, cb.strv, cb.tok0, lane);
-  // bitmap words (K layout: word t of tokens g, g+8)
-  const bool v0 = g < cb.nvalid, v1 = g + 8 < cb.nvalid;
-  const uint32_t kw0 = v0 ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
-  const uint32_t kw1 = v1 ? ld_s32(smem, cb.kbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
-  const uint32_t vw0 = v0 ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g) + 4 * t) : 0u;
-  const uint32_t vw1 = v1 ? ld_s32(smem, cb.vbm + 16 * (cb.tok0 + g + 8) + 4 * t) : 0u;
-  // exclusive prefix (over t) of word popcounts, two tokens packed in 16-bit halves
-  const uint32_t pk = __popc(kw0) | (__popc(kw1) << 16), pv = __popc(vw0) | (__popc(vw1) << 16);
-  uint32_t ik = pk, iv = pv;
-#pragma unroll
-  for (int o = 1; o < 4; o <<= 1) {
-    const uint32_t yk = __shfl_up_sync(0xffffffffu, ik, o, 4), yv = __shfl_up_sync(0xffffffffu, iv, o, 4);
-    if (t >= o) { ik += yk; iv += yv; }
-  }
-  const uint32_t ek = ik - pk, ev = iv - pv;
-  __syncwarp();
-  // K operand
-  const uint32_t bk0 = cb.yk + (uint32_t)g * cb.strk + 12 + 4 * (ek & 0xFFFF);
-  const uint32_t bk1 = bk0 + 8 * cb.strk + 4 * ((ek >> 16) - (ek & 0xFFFF));
-  gather_word16(smem, kw0, bk0, r.k[0]);
-  gather_word16(smem, kw1, bk1, r.k[1]);
-  // V operand: word g/2 (half g%2) of tokens 2t, 2t+1, 2t+8, 2t+9, fetched from the K-layout lanes
-  const int sa = 8 * t + (g >> 1), sb = sa + 4, hsh = 16 * (g & 1);
-  const uint32_t w2t = __shfl_sync(0xffffffffu, vw0, sa), w2t8 = __shfl_sync(0xffffffffu, vw1, sa);
-  const uint32_t w2t1 = __shfl_sync(0xffffffffu, vw0, sb), w2t9 = __shfl_sync(0xffffffffu, vw1, sb);
-  const uint32_t pa = __shfl_sync(0xffffffffu, ev, sa), pb = __shfl_sync(0xffffffffu, ev, sb);
-  const uint32_t ws[4] = {w2t, w2t1, w2t8, w2t9};
-  const uint32_t ps[4] = {pa & 0xFFFF, pb & 0xFFFF, pa >> 16, pb >> 16};
-  const int tk[4] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9};
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const uint32_t extra = (g & 1) ? __popc(ws[x] & 0xFFFFu) : 0u;
-    const uint32_t base = cb.yv + (uint32_t)tk[x] * cb.strv + 12 + 4 * (ps[x] + extra);
-    gather_half8(smem, ws[x] >> hsh, base, r.v[x]);
-  }
-}
-
 // K half: pair arrays of the 16 K tokens, then the K operand (k[2][16]).
 template <int NK>
 __device__ __forceinline__ void fill_k(const CompBlock& cb, uint8_t* smem, uint32_t (&kr)[2][16], int lane) {
