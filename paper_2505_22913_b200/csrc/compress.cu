@@ -39,7 +39,10 @@ __global__ void set_counters_uniform(int32_t* n_comp, int32_t* n_win, int U, int
 // Grid (ceil(T / (8 * 4 * kPrefillGroups)), min(2U, 65535)): row = tensor * U + unit (strided by
 // gridDim.y); warp w of block x handles token groups of 4 starting at (8x + w) * 4 * kPrefillGroups.
 // Control flow is warp-uniform (a token past the row's end computes on zeros and stores nothing).
-constexpr int kPrefillGroups = 4;  // 4-token groups per warp
+#ifndef MSTF_PREFILL_GROUPS
+#define MSTF_PREFILL_GROUPS 8
+#endif
+constexpr int kPrefillGroups = MSTF_PREFILL_GROUPS;  // 4-token groups per warp
 #ifndef MSTF_PREFILL_HSET
 #define MSTF_PREFILL_HSET 1
 #endif
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
       n0 = __ldcs(src + (size_t)(g0 + q) * (kD / 8));
       n1 = __ldcs(src + (size_t)(g0 + q) * (kD / 8) + 1);
     }
+    int pred_hb = -1;  // bits 14..8 of this slot's previous tau (-1: none yet)
     for (int gt = g0; gt < gend; gt += 4) {
       const int t = gt + q;
       const bool valid = t < gend;
@@ -108,16 +112,40 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
       uint32_t hb[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) hb[i] = __byte_perm(w[2 * i], w[2 * i + 1], 0x7531) | 0x80808080u;
-      uint32_t t4 = 0;  // bits 14..8 of tau, replicated in 4 bytes
-#pragma unroll
-      for (int b = 6; b >= 0; --b) {
-        const uint32_t c4 = t4 | (0x01010101u << b);
+      // #{mag >> 8 >= c} for this lane's token, c replicated in the 4 bytes of c4 (c <= 0x7F)
+      auto count_hb = [&](uint32_t c4) {
         uint32_t f = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) f = __umulhi((hb[i] - c4) & 0x80808080u, 1u << 25) + f;  // byte counts
-        const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x01010101u, 0, put3)), 0, take);
-        t4 = cnt >= kk ? c4 : t4;
+        return __byte_perm(warp_sum(__byte_perm(f * 0x01010101u, 0, put3)), 0, take);
+      };
+      uint32_t t4 = 0;  // bits 14..8 of tau, replicated in 4 bytes
+      bool searched = false;
+      if (gt != g0) {  // warp-uniform; a slot valid now was valid in every earlier group
+        // bracket from the previous group's token in this slot (neighbouring tokens of one head
+        // have similar magnitude distributions): T8 in [L, L + 3] iff #{>= L} >= k and
+        // #{>= L + 4} < k; then two steps instead of seven. Exact either way (fallback below).
+        const uint32_t L = (uint32_t)min(max(pred_hb - 1, 0), 123);
+        // both warp sums on every lane (no short-circuit: the reductions need the whole warp)
+        const uint32_t n_lo = count_hb(L * 0x01010101u), n_hi = count_hb((L + 4) * 0x01010101u);
+        const bool ok = !valid || (n_lo >= kk && n_hi < kk);
+        if (__all_sync(0xffffffffu, ok)) {
+          t4 = L * 0x01010101u;
+          uint32_t c4 = t4 + 0x02020202u;
+          t4 = count_hb(c4) >= kk ? c4 : t4;
+          c4 = t4 + 0x01010101u;
+          t4 = count_hb(c4) >= kk ? c4 : t4;
+          searched = true;
+        }
       }
+      if (!searched) {
+#pragma unroll
+        for (int b = 6; b >= 0; --b) {
+          const uint32_t c4 = t4 | (0x01010101u << b);
+          t4 = count_hb(c4) >= kk ? c4 : t4;
+        }
+      }
+      pred_hb = valid ? (int)(t4 & 0x7Fu) : pred_hb;
       uint32_t t2 = (t4 & 0x7Fu) * 0x01000100u;  // tau, replicated in 2 halves
 #if MSTF_PREFILL_HSET
       // bits 7..0 with fp16 compares: a magnitude is a non-negative fp16 value, and for those the
