@@ -152,6 +152,8 @@ def check_attention(M, gc, oc, U_b, hq, hkv, seed, scale=None, qkind="normal", o
     (2, 4, 4, 1000, 39, 39, 32),        # MHA, several chunks, ragged tail
     (2, 32, 8, 777, 39, 39, 32),        # GQA G=4
     (1, 8, 1, 3000, 64, 26, 32),        # G=8, K != V sparsity
+    (1, 8, 1, 3000, 39, 39, 32),        # G=8, one unit: stream-K combine with 2 sub-warps per head
+    (1, 1, 1, 3000, 39, 39, 32),        # G=1, one unit: combine with 4 sub-warps per head
     (3, 2, 1, 129, 128, 128, 32),       # sparsity 0 (dense through the sparse path)
     (1, 4, 2, 20, 39, 39, 32),          # window only (no compressed tokens)
     (2, 4, 2, 5000, 13, 13, 1),         # 90% sparsity, W = 1
