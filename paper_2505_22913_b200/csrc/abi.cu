@@ -44,6 +44,11 @@ int sm_count() {
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+// The combine kernels store 4 outputs per lane: one float4 (f32) or two half2 (f16, 8 bytes).
+inline bool out_aligned(const void* out, int32_t out_dtype) {
+  return out_dtype == MSTF_OUT_F16 ? aligned8(out) : aligned16(out);
+}
 
 }  // namespace
 
@@ -192,6 +197,7 @@ int check_attention_args(const mstf_cache* h, const void* q, const void* out, in
                          size_t ws_bytes) {
   if (!h || !q || !out || !aligned16(q)) return MSTF_EINVAL;
   if (out_dtype != MSTF_OUT_F32 && out_dtype != MSTF_OUT_F16) return MSTF_EINVAL;
+  if (!out_aligned(out, out_dtype)) return MSTF_EINVAL;
   if (!ws || !aligned16(ws) || ws_bytes < mstf_workspace_bytes(h)) return MSTF_EWORKSPACE;
   return MSTF_OK;
 }
@@ -332,7 +338,12 @@ int mstf_dense_decode_attention(const void* k, const void* v, const int32_t* len
   if (head_dim % 64 != 0) return MSTF_ESHAPE;
   if (head_dim != kD || group > kMaxGroup) return MSTF_ENOTSUP;
   if (out_dtype != MSTF_OUT_F32 && out_dtype != MSTF_OUT_F16) return MSTF_EINVAL;
-  if (!ws || ws_bytes < mstf_dense_workspace_bytes(units, group, head_dim, t_max)) return MSTF_EWORKSPACE;
+  // uint4 loads of k / v / q rows, float4 partials in the workspace, vector stores of out
+  if (!aligned16(k) || !aligned16(v) || !aligned16(q) || !out_aligned(out, out_dtype) ||
+      (reinterpret_cast<uintptr_t>(lengths) & 3u))
+    return MSTF_EINVAL;
+  if (!ws || !aligned16(ws) || ws_bytes < mstf_dense_workspace_bytes(units, group, head_dim, t_max))
+    return MSTF_EWORKSPACE;
   if (launch_dense_attention(static_cast<const uint16_t*>(k), static_cast<const uint16_t*>(v), lengths, units,
                              group, t_max, dense_splits(units, t_max), static_cast<const uint16_t*>(q), scale, out,
                              out_dtype == MSTF_OUT_F16, ws, static_cast<cudaStream_t>(stream)) != cudaSuccess)

@@ -147,37 +147,41 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
       }
       pred_hb = valid ? (int)(t4 & 0x7Fu) : pred_hb;
       uint32_t t2 = (t4 & 0x7Fu) * 0x01000100u;  // tau, replicated in 2 halves
-#if MSTF_PREFILL_HSET
       // bits 7..0 with fp16 compares: a magnitude is a non-negative fp16 value, and for those the
-      // order of the values is the order of the bit patterns (candidates >= 0x7C01 are NaNs and
-      // compare false, like every finite magnitude against them). __hge2 gives 1.0 / 0.0 per
-      // half; the sum starts at 1024.0, where the fp16 spacing is 1, so its bits are
-      // 0x6400 + count per half.
-      __half2 xm[8];
+      // order of the values is the order of the bit patterns. Magnitudes are clamped to 0x7C00
+      // (+inf) first, so a NaN channel (0x7C01..0x7FFF, the largest magnitudes under R3) still
+      // compares >= every finite candidate, as it does in the integer phase and the keep mask.
+      // Candidates above 0x7C00 exist only when tau's high byte is >= 0x7C (k or more inf/NaN
+      // channels in a token); fp16 compares cannot rank NaN patterns, so the warp then takes
+      // the integer path (warp-uniform). __hge2 gives 1.0 / 0.0 per half; the sum starts at
+      // 1024.0, where the fp16 spacing is 1, so its bits are 0x6400 + count per half.
+      const bool int_path = !MSTF_PREFILL_HSET || __any_sync(0xffffffffu, (t4 & 0x7Fu) >= 0x7Cu);
+      if (!int_path) {
+        __half2 xm[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) xm[i] = __ushort2_as_half2(w[i] & 0x7FFF7FFFu);
+        for (int i = 0; i < 8; ++i) xm[i] = __ushort2_as_half2(__vminu2(w[i] & 0x7FFF7FFFu, 0x7C007C00u));
 #pragma unroll
-      for (int b = 7; b >= 0; --b) {
-        const uint32_t c2 = t2 | (0x00010001u << b);
-        const __half2 ch = __ushort2_as_half2(c2);
-        __half2 acc = __ushort2_as_half2(0x64006400u);
+        for (int b = 7; b >= 0; --b) {
+          const uint32_t c2 = t2 | (0x00010001u << b);
+          const __half2 ch = __ushort2_as_half2(c2);
+          __half2 acc = __ushort2_as_half2(0x64006400u);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc = __hadd2(acc, __hge2(xm[i], ch));
-        const uint32_t f = __half2_as_u32(acc) - 0x64006400u;  // half counts
-        const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x00010001u, 0, put2)), 0, take);
-        t2 = cnt >= kk ? c2 : t2;
+          for (int i = 0; i < 8; ++i) acc = __hadd2(acc, __hge2(xm[i], ch));
+          const uint32_t f = __half2_as_u32(acc) - 0x64006400u;  // half counts
+          const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x00010001u, 0, put2)), 0, take);
+          t2 = cnt >= kk ? c2 : t2;
+        }
+      } else {
+#pragma unroll 1
+        for (int b = 7; b >= 0; --b) {
+          const uint32_t c2 = t2 | (0x00010001u << b);
+          uint32_t f = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f = __umulhi((ax[i] - c2) & 0x80008000u, 1u << 17) + f;  // half counts
+          const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x00010001u, 0, put2)), 0, take);
+          t2 = cnt >= kk ? c2 : t2;
+        }
       }
-#else
-#pragma unroll
-      for (int b = 7; b >= 0; --b) {
-        const uint32_t c2 = t2 | (0x00010001u << b);
-        uint32_t f = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) f = __umulhi((ax[i] - c2) & 0x80008000u, 1u << 17) + f;  // half counts
-        const uint32_t cnt = __byte_perm(warp_sum(__byte_perm(f * 0x00010001u, 0, put2)), 0, take);
-        t2 = cnt >= kk ? c2 : t2;
-      }
-#endif
       // keep mask of the lane's 16 channels: bit j <-> channel 16r + j (mag >= tau)
       uint32_t acc = 0;
 #pragma unroll
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_
         }
         above = incl - above;
         if (valid && ge > kk) {
-          const uint32_t need = kk - ngt;
+          const uint32_t need = ngt < kk ? kk - ngt : 0u;  // ngt <= kk when tau is exact
           uint32_t keep_eq = 0;
 #pragma unroll
           for (int j = 15; j >= 0; --j) {

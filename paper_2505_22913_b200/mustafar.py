@@ -110,6 +110,16 @@ def _dev_ptr(t: torch.Tensor, dtype=torch.float16, name="tensor") -> int:
     return t.data_ptr()
 
 
+def _expect(t: torch.Tensor, shape, name: str):
+    """Shape guard before a pointer crosses the C ABI (the library sees only pointers and
+    sizes, so a wrong-sized tensor would be read or written out of bounds on the device)."""
+    if tuple(t.shape) != tuple(shape):
+        # accept any view with the same element count and contiguous layout ([B, H, d] == [U, G, d])
+        if t.numel() != math.prod(shape):
+            raise ValueError(f"{name}: expected shape {tuple(shape)} ({math.prod(shape)} elements), "
+                             f"got {tuple(t.shape)}")
+
+
 def keep_from_sparsity(s: float, d: int) -> int:
     return int(lib().mstf_keep_from_sparsity(float(s), int(d)))
 
@@ -130,6 +140,7 @@ def query_abs_sum(q: torch.Tensor, out: torch.Tensor | None = None, stream=None)
     U, R, G, d = q.shape
     if out is None:
         out = torch.empty(U, d, dtype=torch.float32, device=q.device)
+    _expect(out, (U, d), "out")
     _check("mstf_query_abs_sum", lib().mstf_query_abs_sum(_dev_ptr(q, name="q"), U, R, G, d,
                                                           _dev_ptr(out, torch.float32, "out"), _stream(stream)))
     return out
@@ -146,6 +157,7 @@ def merge_partials(ml: torch.Tensor, o: torch.Tensor, out=None, out_dtype=torch.
     """Merge shard partials ml float32 [n, U, G, 2], o float32 [n, U, G, d] -> out [U, G, d]
     (mstf_merge_partials)."""
     n, U, G, d = o.shape
+    _expect(ml, (n, U, G, 2), "ml")
     if out is None:
         out = torch.empty(U, G, d, dtype=out_dtype, device=o.device)
     code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
@@ -253,8 +265,13 @@ class MustafarCache:
     def prune_compress_kv(self, k: torch.Tensor, v: torch.Tensor, lengths=None, stream=None):
         """k, v: fp16 [U, T, d] (== [B, Hkv, T, d]) on the device."""
         T = k.shape[-2]
+        d = self.shape.head_dim
+        _expect(k, (self.units, T, d), "k")
+        _expect(v, (self.units, T, d), "v")
         ln = None
         if lengths is not None:
+            if len(lengths) != self.units:
+                raise ValueError(f"lengths: expected {self.units} entries, got {len(lengths)}")
             ln = (ctypes.c_int32 * self.units)(*[int(x) for x in lengths])
         _check("mstf_prune_compress_kv",
                lib().mstf_prune_compress_kv(self._h, _dev_ptr(k, name="k"), _dev_ptr(v, name="v"), T, ln,
@@ -266,10 +283,13 @@ class MustafarCache:
         (mstf_sparse_decode_attention_partial)."""
         d, U, G = self.shape.head_dim, self.units, self.shape.group
         scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+        _expect(q, (U, G, d), "q")
         if ml is None:
             ml = torch.empty(U, G, 2, dtype=torch.float32, device=self.device)
         if o is None:
             o = torch.empty(U, G, d, dtype=torch.float32, device=self.device)
+        _expect(ml, (U, G, 2), "ml")
+        _expect(o, (U, G, d), "o")
         _check("mstf_sparse_decode_attention_partial",
                lib().mstf_sparse_decode_attention_partial(self._h, _dev_ptr(q, name="q"), scale,
                                                           _dev_ptr(ml, torch.float32, "ml"),
@@ -281,12 +301,16 @@ class MustafarCache:
         """Output-aware K pruning for later K compressions: w float32 [U, d] on the device
         (read by the kernels at run time; keep it alive and update it in stream order), or None
         for magnitude pruning (mstf_set_key_weights)."""
+        if w is not None:
+            _expect(w, (self.units, self.shape.head_dim), "w")
         ptr = None if w is None else _dev_ptr(w, torch.float32, "w")
         _check("mstf_set_key_weights", lib().mstf_set_key_weights(self._h, ptr))
         self._kw = w
 
     def append_token(self, k_new: torch.Tensor, v_new: torch.Tensor, stream=None):
         """k_new, v_new: fp16 [U, d] (== [B, Hkv, d]) on the device."""
+        _expect(k_new, (self.units, self.shape.head_dim), "k_new")
+        _expect(v_new, (self.units, self.shape.head_dim), "v_new")
         _check("mstf_append_token", lib().mstf_append_token(self._h, _dev_ptr(k_new, name="k_new"),
                                                            _dev_ptr(v_new, name="v_new"), _stream(stream)))
 
@@ -296,8 +320,12 @@ class MustafarCache:
         cache is uniform (mstf_decode_step). Returns out [U, G, d]."""
         d = self.shape.head_dim
         scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+        _expect(k_new, (self.units, d), "k_new")
+        _expect(v_new, (self.units, d), "v_new")
+        _expect(q, (self.units, self.shape.group, d), "q")
         if out is None:
             out = torch.empty((self.units, self.shape.group, d), dtype=out_dtype, device=self.device)
+        _expect(out, (self.units, self.shape.group, d), "out")
         code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
         _check("mstf_decode_step",
                lib().mstf_decode_step(self._h, _dev_ptr(k_new, name="k_new"), _dev_ptr(v_new, name="v_new"),
@@ -317,8 +345,10 @@ class MustafarCache:
         """q: fp16 [U, G, d] (== [B, Hq, d]). Returns out [U, G, d] (fp32 or fp16)."""
         d = self.shape.head_dim
         scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+        _expect(q, (self.units, self.shape.group, d), "q")
         if out is None:
             out = torch.empty((self.units, self.shape.group, d), dtype=out_dtype, device=self.device)
+        _expect(out, (self.units, self.shape.group, d), "out")
         code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
         _check("mstf_sparse_decode_attention",
                lib().mstf_sparse_decode_attention(self._h, _dev_ptr(q, name="q"), scale,
@@ -340,8 +370,14 @@ class DenseAttention:
 
     def __call__(self, k, v, lengths, q, scale=None, out=None, out_dtype=torch.float32, stream=None):
         scale = 1.0 / math.sqrt(self.head_dim) if scale is None else float(scale)
+        U, G, d = self.units, self.group, self.head_dim
+        _expect(k, (U, self.t_max, d), "k")
+        _expect(v, (U, self.t_max, d), "v")
+        _expect(lengths, (U,), "lengths")
+        _expect(q, (U, G, d), "q")
         if out is None:
-            out = torch.empty((self.units, self.group, self.head_dim), dtype=out_dtype, device=self.device)
+            out = torch.empty((U, G, d), dtype=out_dtype, device=self.device)
+        _expect(out, (U, G, d), "out")
         code = OUT_F16 if out.dtype == torch.float16 else OUT_F32
         _check("mstf_dense_decode_attention",
                lib().mstf_dense_decode_attention(_dev_ptr(k, name="k"), _dev_ptr(v, name="v"),

@@ -26,6 +26,22 @@ def M():
     return mustafar
 
 
+def compare_unit(bufs, u, oc, note):
+    """Every record buffer of unit u (bitmaps, packed values, tile offsets of K and V), the
+    window ring and both counters, bit-exact against the oracle's one-unit cache."""
+    nc, nw = int(oc.n_comp[0]), int(oc.n_win[0])
+    assert int(bufs["n_comp"][u]) == nc and int(bufs["n_win"][u]) == nw, note
+    for name, dt in (("bitmap_k", np.uint64), ("bitmap_v", np.uint64), ("values_k", np.uint16),
+                     ("values_v", np.uint16), ("offsets_k", np.uint32), ("offsets_v", np.uint32)):
+        g = bufs[name][u, :nc].cpu().numpy().view(dt)
+        assert np.array_equal(g, getattr(oc, name)[0, :nc]), (note, name)
+    if oc.W:
+        slots = [(nc + i) % oc.W for i in range(nw)]
+        for name in ("win_k", "win_v"):
+            g = bufs[name][u].cpu().numpy().view(np.uint16)
+            assert np.array_equal(g[slots], getattr(oc, name)[0, slots]), (note, name)
+
+
 CASES = {
     # name: (batch, hq, hkv, T, sparsity_k, sparsity_v, sampled units)
     "C2_b16_s70": (16, 32, 8, 4096, 0.7, 0.7, (0, 77, 127)),
@@ -57,21 +73,18 @@ def test_fullsize_sampled(M, name):
         Vu = synth.fp16_np_rows((U, T, d), sV, u * T, T).view(np.uint16)
         oc = O.OracleCache(1, d, kk, kv, W, T)
         oc.prefill(Ku[None], Vu[None])
-        nc = int(oc.n_comp[0])
-        # format, bit-exact, for the sampled unit
-        assert np.array_equal(bufs["bitmap_k"][u, :nc].cpu().numpy().view(np.uint64), oc.bitmap_k[0, :nc])
-        assert np.array_equal(bufs["values_v"][u, :nc].cpu().numpy().view(np.uint16), oc.values_v[0, :nc])
-        assert np.array_equal(bufs["offsets_k"][u, :nc].cpu().numpy().view(np.uint32), oc.offsets_k[0, :nc])
+        compare_unit(bufs, u, oc, f"{name} u={u}")
         ref = O.attention(oc, qh[u][None], 1 / math.sqrt(d))[0]
         o = out[u].cpu().numpy().astype(np.float64)
         err = float((np.abs(o - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max())
         assert err <= TOL, (name, u, err)
 
 
-@pytest.mark.parametrize("name", ["C2_b16_s70", "C4_128k_b8"])
+@pytest.mark.parametrize("name", ["C2_b16_s70", "C3_mha_32k", "C4_128k_b8", "C5_16k_b64"])
 def test_fullsize_decode_step_sampled(M, name):
     """One fused decode step (mstf_decode_step: the append inside the attention launch) at full
-    size, against the oracle on sampled units."""
+    size -- the launch configuration bench.py times -- against the oracle on sampled units:
+    every record buffer, the window and the counters bit-exact, attention within 2e-3."""
     B, hq, hkv, T, sk, sv, sample = CASES[name]
     U, G, d, W = B * hkv, hq // hkv, 128, 32
     kk, kv = O.keep_count(sk, d), O.keep_count(sv, d)
@@ -86,6 +99,7 @@ def test_fullsize_decode_step_sampled(M, name):
     assert gc.decode_step_kernel_count() == 2
     out = gc.decode_step(kn, vn, q, 1 / math.sqrt(d))
     torch.cuda.synchronize()
+    bufs = gc.buffers()
     qh = q.cpu().view(torch.int16).numpy().view(np.uint16)
     for u in sample:
         Ku = synth.fp16_np_rows((U, T + 1, d), sK, u * (T + 1), T + 1).view(np.uint16)
@@ -93,6 +107,7 @@ def test_fullsize_decode_step_sampled(M, name):
         oc = O.OracleCache(1, d, kk, kv, W, T + 1)
         oc.prefill(Ku[None, :T], Vu[None, :T])
         oc.append(Ku[None, T], Vu[None, T])
+        compare_unit(bufs, u, oc, f"{name} step u={u}")
         ref = O.attention(oc, qh[u][None], 1 / math.sqrt(d))[0]
         o = out[u].cpu().numpy().astype(np.float64)
         err = float((np.abs(o - ref).max(axis=-1) / np.abs(ref).max(axis=-1)).max())
@@ -125,10 +140,7 @@ def test_fullsize_output_aware_prefill_sampled(M):
         oc = O.OracleCache(1, d, kk, kk, W, T)
         oc.set_key_weights(wh[u][None])
         oc.prefill(Ku[None], Vu[None])
-        nc = int(oc.n_comp[0])
-        assert np.array_equal(bufs["bitmap_k"][u, :nc].cpu().numpy().view(np.uint64), oc.bitmap_k[0, :nc])
-        assert np.array_equal(bufs["values_k"][u, :nc].cpu().numpy().view(np.uint16), oc.values_k[0, :nc])
-        assert np.array_equal(bufs["bitmap_v"][u, :nc].cpu().numpy().view(np.uint64), oc.bitmap_v[0, :nc])
+        compare_unit(bufs, u, oc, f"output-aware u={u}")
 
 
 def test_fullsize_sequence_split_sampled(M):

@@ -86,6 +86,38 @@ def test_prefill_bit_exact(M, kind, kk, kv):
     compare_cache(gc, oc, f"{kind} k={kk},{kv}")
 
 
+@pytest.mark.parametrize("kk", [39, 64, 2])
+def test_prefill_and_append_inf_nan_channels(M, kk):
+    """Tokens with +-inf and NaN channels (R3: |x| is bits & 0x7FFF as an unsigned integer, so
+    NaN patterns rank above inf, inf above every finite value). Records stay bit-exact with the
+    oracle -- in particular exactly k channels kept per token, also when several NaNs sit in one
+    token (the prefill's fp16-compare phase once undercounted them) or when k or more
+    channels of a token are inf/NaN (the integer fallback)."""
+    U_b, hkv, T = 1, 2, 80
+    U = U_b * hkv
+    K = synth.fp16_np((U, T + 4, 128), 4242)
+    V = synth.fp16_np((U, T + 4, 128), 4243)
+    rng = np.random.default_rng(kk)
+    specials = np.array([0x7C00, 0xFC00, 0x7E00, 0xFE00, 0x7C01, 0x7FFF, 0x7D55], dtype=np.uint16)
+    for arr in (K, V):
+        a = arr.view(np.uint16)
+        for u in range(U):
+            for t in range(T + 4):
+                n = [0, 1, 2, 3, 5, 40, 70][t % 7]   # 40 / 70 >= k for most k: integer fallback
+                ch = rng.choice(128, size=n, replace=False)
+                a[u, t, ch] = rng.choice(specials, size=n)
+    gc = M.MustafarCache(U_b, 4, hkv, 128, kk, kk, 8, T + 4)
+    oc = O.OracleCache(U, 128, kk, kk, 8, T + 4)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).cuda().view(torch.float16)
+    gc.prune_compress_kv(dev(K[:, :T]), dev(V[:, :T]))
+    oc.prefill(K[:, :T].view(np.uint16), V[:, :T].view(np.uint16))
+    for i in range(4):
+        gc.append_token(dev(K[:, T + i]), dev(V[:, T + i]))
+        oc.append(K[:, T + i].view(np.uint16), V[:, T + i].view(np.uint16))
+    torch.cuda.synchronize()
+    compare_cache(gc, oc, f"inf/nan k={kk}")
+
+
 @pytest.mark.parametrize("W", [0, 1, 5, 32, 64])
 def test_prefill_windows_and_ragged(M, W):
     lengths = [0, 1, W, W + 1, 200, 137, 64, 3]
@@ -269,6 +301,9 @@ def _twin_caches(M, U_b, hq, hkv, T, kk, kv, W, steps, lengths=None, seed=11):
     (1, 8, 2, 300, 64, 64, 32, 3, None),        # k_pad 64 (register kernel, vector loads): fused
     (1, 8, 2, 300, 26, 39, 32, 3, None),        # K != V sparsity (TMA kernel): unfused
     (200, 16, 8, 40, 39, 39, 32, 2, None),      # 1600 units > 1184 workers (appends loop)
+    (2, 4, 4, 500, 39, 39, 32, 4, None),        # G = 1 (MHA, the C3 shape): fused
+    (1, 1, 1, 3000, 39, 39, 32, 3, None),       # G = 1, one unit: fused, many workers per unit
+    (3, 6, 3, 200, 39, 39, 32, 3, None),        # G = 2
 ])
 def test_decode_step_equals_append_then_attention(M, case):
     U_b, hq, hkv, T, kk, kv, W, steps, lengths = case

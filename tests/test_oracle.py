@@ -273,6 +273,52 @@ def test_pruned_attention_equals_sdpa_on_zero_filled():
         np.testing.assert_allclose(out[u], _sdpa64(q[u], Kp, Vp, 0.1), rtol=1e-12, atol=1e-14)
 
 
+@pytest.mark.parametrize("n,G", [(1, 1), (64, 4), (333, 8)])
+def test_attention_dense_equals_sdpa_float64(n, G):
+    """attention_dense (the checker of the dense-KV baseline kernel) is textbook attention:
+    pinned to torch SDPA in float64 (a library routine), including n = 1 (-> v0)."""
+    d = 128
+    K = synth.fp16_np((n, d), 71 + n).view(np.uint16)
+    V = synth.fp16_np((n, d), 72 + n).view(np.uint16)
+    q = synth.fp16_np((G, d), 73 + n).view(np.uint16)
+    for scale in (1 / math.sqrt(d), 0.7):
+        np.testing.assert_allclose(O.attention_dense(q, K, V, scale), _sdpa64(q, K, V, scale),
+                                   rtol=1e-12, atol=1e-14)
+    if n == 1:
+        assert np.array_equal(O.attention_dense(q, K, V, 0.1), np.broadcast_to(O.fp16_to_f64(V[0]), (G, d)))
+
+
+@pytest.mark.parametrize("W", [0, 5, 400])
+def test_attention_dense_equals_cache_attention_unpruned(W):
+    """With keep = d nothing is pruned, so Alg. 1 over the compressed cache (any window,
+    including W >= T: all tokens dense) equals attention_dense over the raw K/V."""
+    U, T, d, G = 2, 130, 128, 4
+    K = synth.fp16_np((U, T, d), 81).view(np.uint16)
+    V = synth.fp16_np((U, T, d), 82).view(np.uint16)
+    q = synth.fp16_np((U, G, d), 83).view(np.uint16)
+    c = O.OracleCache(U, d, d, d, W, capacity=T)
+    c.prefill(K, V)
+    out = O.attention(c, q, 1 / math.sqrt(d))
+    for u in range(U):
+        np.testing.assert_allclose(out[u], O.attention_dense(q[u], K[u], V[u], 1 / math.sqrt(d)),
+                                   rtol=1e-12, atol=1e-14)
+
+
+def test_attention_dense_shift_and_permutation():
+    """Invariants of softmax(scale q K^T) V that a transposed operand or a normalisation over
+    the wrong axis would break: scale 0 gives the mean of V for every head, and permuting the
+    tokens (K and V rows together) leaves the output unchanged."""
+    n, d, G = 50, 128, 2
+    K = synth.fp16_np((n, d), 91).view(np.uint16)
+    V = synth.fp16_np((n, d), 92).view(np.uint16)
+    q = synth.fp16_np((G, d), 93).view(np.uint16)
+    np.testing.assert_allclose(O.attention_dense(q, K, V, 0.0),
+                               np.broadcast_to(O.fp16_to_f64(V).mean(axis=0), (G, d)), rtol=1e-13, atol=1e-15)
+    perm = np.random.default_rng(3).permutation(n)
+    np.testing.assert_allclose(O.attention_dense(q, K[perm], V[perm], 0.3), O.attention_dense(q, K, V, 0.3),
+                               rtol=1e-12, atol=1e-14)
+
+
 def test_spmv_score_golden():
     g = GOLD["spmv_score"]
     row = np.zeros(g["d"], np.float16)

@@ -133,3 +133,55 @@ def test_cache_key_weights_change_k_only():
     c.set_key_weights(np.ones((U, d), np.float32))
     c.prefill(K, V)
     assert np.array_equal(c.bitmap_k, b.bitmap_k) and np.array_equal(c.values_k, b.values_k)
+
+
+def _keep_f64(bits, w, k):
+    """The same top-k (R2 ties) on float64 scores |k| * w -- exact products."""
+    s64 = np.abs(bits.view(np.float16).astype(np.float64)) * np.asarray(w, np.float32).astype(np.float64)
+    idx = np.broadcast_to(np.arange(bits.shape[-1]), s64.shape)
+    order = np.lexsort((idx, s64), axis=-1)
+    keep = np.ones(s64.shape, bool)
+    np.put_along_axis(keep, order[..., : bits.shape[-1] - k], False, axis=-1)
+    return keep, s64
+
+
+def test_scored_selection_constructed_near_tie():
+    """A decision float32 cannot resolve: |3| * (1 + 2^-23) = 3 + 1.5 ulp(3) and |1| * (3 + 2^-21)
+    = 3 + 2 ulp(3) differ in float64 but round to the same float32 score, so R20 (float32) falls
+    back to the tie rule (keep the higher channel, 9) where float64 keeps channel 5. The test
+    below bounds every such difference to this kind of near-tie."""
+    d, k = 16, 4
+    x = np.full(d, 0.001, np.float16)
+    x[[0, 1, 2]] = 100.0
+    x[5], x[9] = 1.0, 3.0
+    w = np.ones(d, np.float32)
+    w[5], w[9] = np.float32(3 + 2 ** -21), np.float32(1 + 2 ** -23)
+    b = x.view(np.uint16)
+    keep32 = O.prune_tokens_scored(O.key_scores(b, w), k)
+    keep64, s64 = _keep_f64(b, w, k)
+    assert keep32[9] and not keep32[5]
+    assert keep64[5] and not keep64[9]
+    assert abs(s64[5] - s64[9]) <= 2.0 ** -23 * s64[5]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_scored_selection_fp32_vs_fp64_differs_only_at_near_ties(seed):
+    """R20 takes the output-aware selection in the kernel's float32. Cross-check against the
+    same selection on float64 scores |k| * w (exact products of an fp16 and a float32 value):
+    every token whose kept set differs must have its k-th and (k+1)-th largest float64 scores
+    within float32 rounding of each other (a near-tie that float32 cannot order), so the
+    float32 reading never changes a decision float64 resolves clearly."""
+    rng = np.random.default_rng(seed)
+    T, d, k = 4000, 128, 39
+    bits = synth.fp16_np((T, d), 700 + seed).view(np.uint16)
+    q = synth.fp16_np((1, 32, 4, d), 800 + seed).view(np.uint16)
+    w = O.query_abs_sum(q)[0]
+    keep32 = O.prune_tokens_scored(O.key_scores(bits, w), k)
+    keep64, s64 = _keep_f64(bits, w, k)
+    diff = np.nonzero((keep32 != keep64).any(axis=1))[0]
+    for t in diff:
+        srt = np.sort(s64[t])[::-1]
+        a, b = srt[k - 1], srt[k]                 # k-th and (k+1)-th largest
+        assert a - b <= 2.0 ** -23 * a * 2, (t, a, b)
+    # the fp32 rounding of a product changes at most a few decisions
+    assert len(diff) < T // 20
