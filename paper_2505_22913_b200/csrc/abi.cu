@@ -164,10 +164,56 @@ int mstf_append_token(mstf_cache* h, const void* k_new, const void* v_new, void*
 
 size_t mstf_workspace_bytes(const mstf_cache* h) {
   if (!h) return 0;
-  return attention_ws_bytes(h->view.U, h->cfg.num_q_heads / h->cfg.num_kv_heads, h->max_splits);
+  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
+  const size_t a = attention_ws_bytes(h->view.U, G, h->max_splits);
+  const size_t b = warp_ws_bytes(h->view.U, G, sm_count());
+  return a > b ? a : b;
 }
 
 namespace {
+// r2 attention kernel (attn_warp.cu) unless MSTF_ATTN=r1 (dev A/B against the round-1 kernels);
+// read once per process.
+bool use_r2(const mstf_cache* h) {
+  static const bool r1 = [] {
+    const char* e = std::getenv("MSTF_ATTN");
+    return e && std::strcmp(e, "r1") == 0;
+  }();
+  return !r1 && warp_kernel_supported(h->cfg.num_q_heads / h->cfg.num_kv_heads);
+}
+
+// Host-mirror summary of the counters as the attention will see them (after == true: after one
+// decode-step append): stream-K total cost, whether every unit is equal, whether one is empty.
+struct MirrorSummary {
+  int64_t total_cost;
+  bool uniform, empty;
+};
+MirrorSummary summarize(const mstf_cache* h, bool after) {
+  const int32_t U = h->view.U, W = h->view.W;
+  MirrorSummary r{0, true, false};
+  for (int32_t u = 0; u < U; ++u) {
+    int32_t nc = h->nc[u], nw = h->nw[u];
+    if (after) {
+      if (W == 0 || nw == W) nc += 1; else nw += 1;
+    }
+    if (nc + nw == 0) r.empty = true;
+    r.total_cost += sk_unit_cost(nc, W);
+    if (h->nc[u] != h->nc[0] || h->nw[u] != h->nw[0]) r.uniform = false;
+  }
+  return r;
+}
+
+int launch_r2(const mstf_cache* h, const MirrorSummary& ms, bool fuse, const void* k_new, const void* v_new,
+              const void* q, float scale, void* out, int32_t out_dtype, float* part_ml, float* part_o, void* ws,
+              void* stream) {
+  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
+  const WarpPlan plan = plan_warp_attention(h->view.U, G, ms.total_cost, h->view.kpad[0], h->view.kpad[1], sm_count());
+  const cudaError_t e = launch_warp_attention(
+      h->view, plan, G, ms.uniform ? 1 : 0, fuse ? 1 : 0, static_cast<const uint16_t*>(q), scale,
+      static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), out, out_dtype == MSTF_OUT_F16,
+      part_ml, part_o, ws, sm_count(), static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MSTF_OK : MSTF_ECUDA;
+}
+
 // Attention plan from the host mirror (counters as they will be when the kernels run).
 int make_plan(const mstf_cache* h, const std::vector<int32_t>& nc, const std::vector<int32_t>& nw, AttnPlan* plan) {
   int32_t max_comp = 0;
@@ -225,6 +271,11 @@ int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale
                                  void* ws, size_t ws_bytes, void* stream) {
   const int st = check_attention_args(h, q, out, out_dtype, ws, ws_bytes);
   if (st != MSTF_OK) return st;
+  if (use_r2(h)) {
+    const MirrorSummary ms = summarize(h, false);
+    if (ms.empty) return MSTF_EEMPTY;
+    return launch_r2(h, ms, false, nullptr, nullptr, q, scale, out, out_dtype, nullptr, nullptr, ws, stream);
+  }
   AttnPlan plan;
   const int sp = make_plan(h, h->nc, h->nw, &plan);
   if (sp != MSTF_OK) return sp;
@@ -246,6 +297,11 @@ int mstf_sparse_decode_attention_partial(const mstf_cache* h, const void* q, flo
   if (all_empty)  // a shard that holds no token of the sequence (e.g. T < world): the merge identity
     return launch_empty_partials(ml, o, h->view.U * G, static_cast<cudaStream_t>(stream)) == cudaSuccess
                ? MSTF_OK : MSTF_ECUDA;
+  if (use_r2(h)) {
+    const MirrorSummary ms = summarize(h, false);
+    if (ms.empty) return MSTF_EEMPTY;
+    return launch_r2(h, ms, false, nullptr, nullptr, q, scale, nullptr, MSTF_OUT_F32, ml, o, ws, stream);
+  }
   AttnPlan plan;
   const int sp = make_plan(h, h->nc, h->nw, &plan);
   if (sp != MSTF_OK) return sp;
@@ -273,6 +329,21 @@ int mstf_decode_step(mstf_cache* h, const void* k_new, const void* v_new, const 
   const int32_t U = h->view.U, W = h->view.W;
   for (int32_t u = 0; u < U; ++u)
     if ((W == 0 || h->nw[u] == W) && h->nc[u] + 1 > h->view.cap) return MSTF_ECAPACITY;
+  if (use_r2(h)) {
+    const MirrorSummary ms = summarize(h, true);  // counters after the append (a4)
+    if (ms.empty) return MSTF_EEMPTY;
+    if (!ms.uniform) {  // ragged cache: the two calls in sequence
+      const int sa = mstf_append_token(h, k_new, v_new, stream);
+      if (sa != MSTF_OK) return sa;
+      return mstf_sparse_decode_attention(h, q, scale, out, out_dtype, ws, ws_bytes, stream);
+    }
+    const int r = launch_r2(h, ms, true, k_new, v_new, q, scale, out, out_dtype, nullptr, nullptr, ws, stream);
+    if (r != MSTF_OK) return r;
+    for (int32_t u = 0; u < U; ++u) {  // the combine kernel advances the device counters the same way
+      if (W == 0 || h->nw[u] == W) h->nc[u] += 1; else h->nw[u] += 1;
+    }
+    return MSTF_OK;
+  }
   // counters after the append (a4)
   const bool uniform = uniform_counters(h);
   std::vector<int32_t> nc = h->nc, nw = h->nw;
@@ -307,6 +378,8 @@ int mstf_decode_step(mstf_cache* h, const void* k_new, const void* v_new, const 
 
 int mstf_decode_step_kernel_count(const mstf_cache* h) {
   if (!h) return MSTF_EINVAL;
+  if (use_r2(h))  // fused: attention (append inside) + combine; ragged: append + prefix + attention + combine
+    return summarize(h, true).uniform ? 2 : 4;
   // mirrors mstf_decode_step: fused (register kernel + combine) or append + attention + combine
   const int32_t U = h->view.U, W = h->view.W;
   std::vector<int32_t> nc = h->nc, nw = h->nw;
@@ -399,6 +472,7 @@ const char* mstf_status_string(int32_t s) {
 
 int mstf_attention_kernel_count(const mstf_cache* h) {
   if (!h) return MSTF_EINVAL;
+  if (use_r2(h)) return summarize(h, false).uniform ? 2 : 3;  // (+ cost prefix) + attention + combine
   // register kernel (stream-K) + stream-K combine, or TMA kernel (split grid) + combine
   return 2;
 }

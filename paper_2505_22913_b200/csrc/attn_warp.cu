@@ -1,0 +1,883 @@
+// attn_warp.cu -- decode attention directly over the compressed cache (Algorithm 1,
+// P:236-261), one self-contained warp per work item: the r2 kernel.
+//
+// Every warp of a persistent grid is an independent stream-K worker:
+//   * its compressed 16-token blocks are streamed from HBM by TMA bulk copies
+//     (cp.async.bulk, four per block: K bitmaps, K values, V bitmaps, V values -- each a
+//     contiguous run of fixed-stride records, R5-R7) into a private 2-stage shared-memory
+//     ring, issued by the warp itself one block ahead, so the only global-load instructions
+//     of the hot loop are those four copies;
+//   * a5 (q.K^T) and a8 (P.V) run on the tensor cores (mma.sync m16n8k16, fp16 x fp16 ->
+//     fp32) with the SAME warp holding both halves, so no K -> V hand-off exists:
+//       scores  S[row][tok] = Q'[row][ch] . K^T[ch][tok]   M = 16 rows = (head, copy) pairs,
+//               N = 8 tokens, K = 16 channels: the B operand of lane (g, t) is token g's
+//               channel pairs of bitmap word t (the lane's own gathers), and the result
+//               C[row g][tok 2t, 2t+1] is exactly what the V step needs in its B operand;
+//       values  O'[pair][(head, parity)] = V'[pair][(tok, e)] . P'[(tok, e)][(head, parity)]
+//               M = 16 channel pairs, K = 8 tokens x 2 parities, N = 4 heads x 2 parities:
+//               P'[(tok, e)][(h, p)] = P[h][tok] if e == p else 0, so every A register is
+//               one token's channel pair (the lane's own gathers, no transposition) and
+//               D[pair][(h, p)] = O[h][2 pair + p];
+//   * a7 online softmax in the log2 domain (exp2, log2e folded into the scale);
+//   * the dense local window (a6) is read with 128-bit loads in the same loop;
+//   * each (worker, unit) segment writes one partial (m, l, o) slot; the combine kernel
+//     (a9) merges a unit's slots -- see mstf_warp_combine_kernel.
+// Expansion ("load as compressed, compute as dense"): each token's packed values are
+// rewritten in shared memory as a shifted pair array Y[m] = (h[m-1], h[m]) (two 16-byte
+// stores per 8 values); channel pair (2j, 2j+1) of a bitmap word with exclusive prefix e is
+// then ONE aligned 32-bit load Y[e + popc(word & bits <= 2j)], masked by the two bitmap bits.
+//
+// Fused decode step (mstf_decode_step, uniform caches): the worker that owns a unit's first
+// cost unit also appends that unit's new token (a4) before its attention work and publishes
+// a ready flag; a worker reading the unit's last record or its window waits for the flag.
+// The appender's index is never higher than a reader's, so in-order CTA dispatch cannot
+// deadlock. Counters are read from the device and NOT written here (the combine kernel
+// writes the post-append counters and clears the flags), so a captured CUDA graph of the
+// step replays correctly.
+#include <cfloat>
+#include <cmath>
+#include <cstdlib>
+
+#include "compress_dev.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace mstf {
+
+namespace {
+
+constexpr int kWNst = 2;          // TMA ring depth per warp (blocks in flight)
+constexpr int kWMaxWarps = 16;    // warps per CTA (one CTA per SM, <= 128 registers per thread)
+constexpr int kWHdrInts = 16;     // workspace header: [0] S (total cost), [1] cost per unit (0: ragged)
+
+struct WParams {
+  CacheView c;
+  const uint16_t* q;      // [U][G][kD]
+  int G;
+  float scale_log2;
+  int np;                 // workers (warps of the grid)
+  int wpc;                // warps per CTA
+  int cs, cw;             // cost model: per-segment start, per window block
+  int uniform;            // every unit has the same counters (closed-form partition)
+  int fuse;               // append inside (uniform caches only)
+  int kpk, kpv;           // k_pad of K and V
+  int stage_bytes, off_kval, off_vbm, off_vval;
+  int swk, swv;           // pair-array stride per token (32-bit words)
+  int warp_bytes;         // per-warp shared-memory region
+  int* hdr;               // workspace header (kWHdrInts ints)
+  int* ready;             // [U] fused step: append done (1), cleared by the combine
+  int* pref;              // [U+1] ragged cost prefix (written by mstf_cost_prefix_kernel)
+  float* ws_o;            // [slots][G][kD] partial o (unnormalised)
+  float* ws_ml;           // [slots][G][2] partial (m, l), log2 domain
+  const uint16_t* k_new;  // fused step: [U][kD]
+  const uint16_t* v_new;
+  // combine
+  void* out;
+  int out_f16;
+  float* part_ml;
+  float* part_o;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  asm("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// Gather only when the dibit keeps a channel (mask != 0): idle lanes take no bank slot.
+__device__ __forceinline__ uint32_t lds_masked(uint32_t a, uint32_t mask) {
+  uint32_t v = 0;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
+               : "+r"(v) : "r"(a), "r"(mask) : "memory");
+  return v & mask;
+}
+__device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_u32(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx_u32(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// Generic-proxy shared reads of a stage must be ordered before the async-proxy (TMA) write
+// that refills it.
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Global data published by another CTA (generic stores + release / acquire) must be visible to
+// a TMA read issued after the acquire.
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
+// Mask for dibit J of a word (channels 2J, 2J+1 -> halves lo, hi): 0xFFFF where kept.
+// cp[s] = w << (7 - s) puts bit 8m+s at the sign bit of byte m; prmt's sign-replicate mode
+// turns the two needed sign bits into byte masks.
+template <int J>
+__device__ __forceinline__ uint32_t dibit_mask(const uint32_t (&cp)[8]) {
+  constexpr int m = J / 4, s0 = 2 * (J % 4);
+  constexpr uint32_t lo = 8 | m, hi = 8 | (4 + m);
+  constexpr uint32_t sel = lo | (lo << 4) | (hi << 8) | (hi << 12);
+  return prmt(cp[s0], cp[s0 + 1], sel);
+}
+
+// Expand the 16 dibits of word w: out[j] = channel pair (2j, 2j+1), zeros where pruned.
+// base = shared address of pair entry e (e = kept channels of the token before this word).
+__device__ __forceinline__ void gather16(uint32_t w, uint32_t base_in, uint32_t (&out)[16]) {
+  const uint32_t base = opaque(base_in);
+  uint32_t cp[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) cp[s] = w * (1u << (7 - s));
+#define MSTF_G(J) out[J] = lds_masked(base + 4u * __popc(w * (1u << (31 - 2 * J))), dibit_mask<J>(cp));
+  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
+  MSTF_G(8) MSTF_G(9) MSTF_G(10) MSTF_G(11) MSTF_G(12) MSTF_G(13) MSTF_G(14) MSTF_G(15)
+#undef MSTF_G
+}
+// Expand 8 dibits of two half-words at once: hw2 = (half-word of token b) << 16 | (half-word
+// of token a); bases of the two tokens' pair entries. outa/outb[j] = channel pair j.
+__device__ __forceinline__ void gather8x2(uint32_t hw2, uint32_t base_a_in, uint32_t base_b_in, uint32_t (&outa)[8],
+                                          uint32_t (&outb)[8]) {
+  const uint32_t base_a = opaque(base_a_in), base_b = opaque(base_b_in);
+  uint32_t cp[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) cp[s] = hw2 * (1u << (7 - s));
+  const uint32_t hb = hw2 >> 16;
+// hw2 << (31 - 2J) keeps exactly the low half-word's bits <= 2J (2J <= 14).
+#define MSTF_G(J)                                                                    \
+  outa[J] = lds_masked(base_a + 4u * __popc(hw2 * (1u << (31 - 2 * J))), dibit_mask<J>(cp)); \
+  outb[J] = lds_masked(base_b + 4u * __popc(hb * (1u << (31 - 2 * J))), dibit_mask<8 + J>(cp));
+  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
+#undef MSTF_G
+}
+
+// Shifted pair arrays of the 16 tokens of one tensor in a stage: token tau's entries
+// Y[m] = (h[m-1], h[m]), m = 0..kp (h[-1] = h[kp] = 0) at ydst + 4 * (tau * SW + m).
+// Task (tau, c) = 8 values: one 16-byte load + the previous word, two 16-byte stores.
+template <int NCH>
+__device__ __forceinline__ void build_pairs(uint32_t raw, uint32_t ydst, int nch_rt, int sw, int lane) {
+  const int nch = NCH ? NCH : nch_rt;
+#pragma unroll
+  for (int task = lane; task < 16 * nch; task += 32) {
+    const int tau = task / nch, c = task - tau * nch;
+    const uint32_t src = raw + (uint32_t)(tau * nch * 16 + 16 * c);
+    const uint4 a = lds128(src);
+    const uint32_t prev = c > 0 ? lds32(src - 4) : 0u;
+    const uint32_t dst = ydst + 4u * (uint32_t)(tau * sw + 8 * c);
+    sts128(dst, prmt(prev, a.x, 0x5432), a.x, prmt(a.x, a.y, 0x5432), a.y);
+    sts128(dst + 16, prmt(a.y, a.z, 0x5432), a.z, prmt(a.z, a.w, 0x5432), a.w);
+    if (c == nch - 1) sts32(dst + 32, prmt(a.w, 0u, 0x5432));
+  }
+}
+
+// ---------------------------------------------------------------- schedule (device side)
+// Cost model of the partition (same as the r1 stream-K schedule): a unit's cost list is
+// [cs start units][one per compressed 16-token block][cw per window block]; worker P owns
+// cost units [P*S/NP, (P+1)*S/NP); an item belongs to the worker holding its first cost unit;
+// segment (P, u) writes partial slot P + u (unique: P + u increases along the monotone path).
+struct Counters {
+  int nc, nw;  // as the attention sees them (after the fused append, if any)
+};
+__device__ __forceinline__ Counters counters_of(const WParams& p, int u) {
+  Counters r;
+  r.nc = p.c.n_comp[u];
+  r.nw = p.c.n_win[u];
+  if (p.fuse) {  // a4: the step's append precedes the attention (R12)
+    if (p.c.W == 0 || r.nw == p.c.W) r.nc += 1; else r.nw += 1;
+  }
+  return r;
+}
+__device__ __forceinline__ int nwb_of(const WParams& p) { return p.c.W > 0 ? (p.c.W + 15) / 16 : 0; }
+__device__ __forceinline__ int cost_of(const WParams& p, int nc) { return p.cs + (nc + 15) / 16 + nwb_of(p) * p.cw; }
+__device__ __forceinline__ int unit_start(const WParams& p, int u, int cpu) { return cpu ? u * cpu : p.pref[u]; }
+// first item whose first cost unit is >= x (x unit-relative)
+__device__ __forceinline__ int item_of_cost(const WParams& p, int x, int nbc) {
+  const int y = x - p.cs;
+  if (y <= 0) return 0;
+  if (y <= nbc) return y;
+  return min(nbc + (y - nbc + p.cw - 1) / p.cw, nbc + nwb_of(p));
+}
+__device__ __forceinline__ int unit_of_cost(const WParams& p, int x, int cpu) {
+  if (cpu) return x / cpu;
+  int lo = 0, hi = p.c.U;  // largest u with start(u) <= x
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (p.pref[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int worker_begin(long long S, int np, int P) { return (int)((long long)P * S / np); }
+
+// Fused step: wait until the unit's append is published (bounded spin: a broken invariant
+// becomes a launch error, not a hung GPU).
+__device__ __forceinline__ void wait_ready(const int* flag) {
+  int v;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v != 0) break;
+    if (it > (1u << 22)) __trap();
+    __nanosleep(64);
+  }
+}
+
+// ---------------------------------------------------------------- the kernel
+// G = 8 holds twice the accumulators and q fragments: at most 8 warps per CTA (<= 255 registers).
+template <int NK, int NV, bool G8>
+__global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mstf_attn_warp_kernel(const WParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const CacheView& c = p.c;
+  const int P = (int)blockIdx.x * p.wpc + warp;
+  // per-warp region: [stages kWNst x stage_bytes][pairs K 16 x swk words][pairs V][mbarriers]
+  const uint32_t wbase = smem_u32(smem) + (uint32_t)(warp * p.warp_bytes);
+  const uint32_t ypk = wbase + (uint32_t)(kWNst * p.stage_bytes);
+  const uint32_t ypv = ypk + 64u * (uint32_t)p.swk;
+  const uint32_t bar0 = ypv + 64u * (uint32_t)p.swv;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kWNst; ++s) mbar_init_u32(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  pdl_launch_dependents();
+  pdl_wait();  // cache, counters, q and the ragged prefix come from earlier kernels in the stream
+
+  // ---- partition (device counters: graph-replay safe)
+  int cpu = 0;  // cost per unit (uniform caches)
+  long long S;
+  if (p.uniform) {
+    cpu = cost_of(p, counters_of(p, 0).nc);
+    S = (long long)c.U * cpu;
+  } else {
+    S = p.pref[c.U];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // for the combine
+    p.hdr[0] = (int)S;
+    p.hdr[1] = cpu;
+  }
+  const int x0 = worker_begin(S, p.np, P), x1 = worker_begin(S, p.np, P + 1);
+
+  // ---- a4 (fused step): append the units whose first cost unit this worker owns
+  if (p.fuse) {
+    for (int u = (x0 + cpu - 1) / cpu; u < c.U && u * cpu < x1; ++u) {
+      const int nc0 = c.n_comp[u], nw0 = c.n_win[u];
+      append_unit_warp(c, 0, u, p.k_new + (size_t)u * kD, nc0, nw0, lane);
+      append_unit_warp(c, 1, u, p.v_new + (size_t)u * kD, nc0, nw0, lane);
+      __syncwarp();
+      __threadfence();
+      if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ready + u), "r"(1) : "memory");
+    }
+  }
+  if (x0 >= x1) return;
+
+  // ---- block streams: producer (TMA issue, one block ahead) and consumer walk the same
+  // sequence of compressed blocks: segment by segment, unit u's blocks [lo, min(hi, nbc)).
+  const int u_first = unit_of_cost(p, x0, cpu);
+  // producer cursor
+  int pu = u_first, pb = 0, pbe = 0, pseq = 0;
+  bool pdone = false;
+  auto seg_bounds = [&](int u, int& lo, int& hi, int& nbc, Counters& cn) {
+    cn = counters_of(p, u);
+    nbc = (cn.nc + 15) / 16;
+    const int us = unit_start(p, u, cpu), ue = unit_start(p, u + 1, cpu);
+    lo = item_of_cost(p, max(x0, us) - us, nbc);
+    hi = item_of_cost(p, min(x1, ue) - us, nbc);
+  };
+  {
+    int lo, hi, nbc;
+    Counters cn;
+    seg_bounds(pu, lo, hi, nbc, cn);
+    pb = lo;
+    pbe = min(hi, nbc);
+  }
+  // advance the producer to its next compressed block (or done)
+  auto p_advance = [&]() {
+    while (!pdone && pb >= pbe) {
+      ++pu;
+      if (pu >= c.U || unit_start(p, pu, cpu) >= x1) { pdone = true; break; }
+      int lo, hi, nbc;
+      Counters cn;
+      seg_bounds(pu, lo, hi, nbc, cn);
+      pb = lo;
+      pbe = min(hi, nbc);
+    }
+  };
+  const size_t kbm_stride = (size_t)kTiles * 8;
+  auto p_issue = [&]() {  // lane 0: TMA of block (pu, pb) into stage pseq % kWNst
+    const Counters cn = counters_of(p, pu);
+    const int tok0 = pb * 16, n = min(16, cn.nc - tok0);
+    if (p.fuse && (c.W == 0 || c.n_win[pu] == c.W) && pb == (cn.nc - 1) / 16) {
+      // this block holds the record the step's append writes: wait for it (TMA = async proxy)
+      wait_ready(p.ready + pu);
+      fence_proxy_async_global();
+    }
+    const int s = pseq % kWNst;
+    const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes), bar = bar0 + 8 * s;
+    const size_t rec = (size_t)pu * c.cap + tok0;
+    const uint32_t bytes_bm = (uint32_t)n * 16, bytes_k = (uint32_t)n * 2 * p.kpk, bytes_v = (uint32_t)n * 2 * p.kpv;
+    mbar_expect_tx_u32(bar, 2 * bytes_bm + bytes_k + bytes_v);
+    bulk_g2s_u32(st, reinterpret_cast<const uint8_t*>(c.bm[0]) + rec * kbm_stride, bytes_bm, bar);
+    bulk_g2s_u32(st + p.off_kval, c.val[0] + rec * p.kpk, bytes_k, bar);
+    bulk_g2s_u32(st + p.off_vbm, reinterpret_cast<const uint8_t*>(c.bm[1]) + rec * kbm_stride, bytes_bm, bar);
+    bulk_g2s_u32(st + p.off_vval, c.val[1] + rec * p.kpv, bytes_v, bar);
+  };
+  p_advance();
+  for (int k = 0; k < kWNst && !pdone; ++k) {
+    if (lane == 0) p_issue();
+    ++pseq;
+    ++pb;
+    p_advance();
+  }
+
+  // ---- consumer state
+  constexpr int NT = G8 ? 2 : 1;  // n-tiles of heads (4 heads each) in the V product
+  uint32_t qa[8][2 * NT];         // score A operand: [k-step][row g: lo pair, hi pair (, rows g+8)]
+  float acc[NT][4][4];            // O'[pair][(head, parity)] per V n-tile, 4 m-tiles
+  float m_[NT], l_[NT];
+  const int h0 = g >> 1;          // the score rows of lane (g, t): head g>>1 (and 4 + g>>1 for G = 8)
+  const uint32_t sel_lo = (g & 1) ? 0x1044u : 0x4410u, sel_hi = (g & 1) ? 0x3244u : 0x4432u;
+  int qu = -1;
+  int cseq = 0;  // compressed blocks consumed
+
+  for (int u = u_first; u < c.U; ++u) {
+    const int us = unit_start(p, u, cpu);
+    if (us >= x1) break;
+    int lo, hi, nbc;
+    Counters cn;
+    seg_bounds(u, lo, hi, nbc, cn);
+    if (lo >= hi) {  // only start-cost units of u in this range: an empty partial (weight 0)
+      if (lane < p.G) *reinterpret_cast<float2*>(p.ws_ml + (((size_t)P + u) * p.G + lane) * 2) = make_float2(-INFINITY, 0.f);
+      continue;
+    }
+    if (u != qu) {  // q of the unit's heads in the score layout
+      qu = u;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int h = h0 + 4 * nt;
+        if (h < p.G) {
+          const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + h) * kD + 32 * t);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint4 x = __ldg(qp + i);
+            qa[2 * i][2 * nt] = x.x; qa[2 * i][2 * nt + 1] = x.y;
+            qa[2 * i + 1][2 * nt] = x.z; qa[2 * i + 1][2 * nt + 1] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < 8; ++s) qa[s][2 * nt] = qa[s][2 * nt + 1] = 0u;
+        }
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      m_[nt] = -INFINITY;
+      l_[nt] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[nt][i][0] = acc[nt][i][1] = acc[nt][i][2] = acc[nt][i][3] = 0.f;
+    }
+    if (lane == 0 && hi > nbc && c.W > 0) {  // window rows are read after the unit's records
+      l2_prefetch(c.win[0] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
+      l2_prefetch(c.win[1] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
+    }
+
+    // a5 + a7 for one block: scores, online softmax, rescale of the accumulators; returns the
+    // B operand of the V product per head tile: bb[ht] = {k-step 0 lo, hi, k-step 1 lo, hi}
+    auto scores = [&](const uint32_t (&kr)[2][16], const bool (&valid)[4], uint32_t (&bb)[NT][4]) {
+      float sc[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          if constexpr (G8)
+            mma16816(sc[nt], qa[s][0], qa[s][2], qa[s][1], qa[s][3], kr[nt][2 * s], kr[nt][2 * s + 1]);
+          else
+            mma16816(sc[nt], qa[s][0], 0u, qa[s][1], 0u, kr[nt][2 * s], kr[nt][2 * s + 1]);
+        }
+      }
+      // x[i]: token {2t, 2t+1, 8+2t, 9+2t}[i] of head h0 (c0, c1) and head 4 + h0 (c2, c3)
+#pragma unroll
+      for (int ht = 0; ht < NT; ++ht) {
+        float x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = valid[i] ? sc[i >> 1][2 * ht + (i & 1)] * p.scale_log2 : -INFINITY;
+        float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+        const float mn = fmaxf(m_[ht], bm);
+        const float alpha = ex2(m_[ht] - mn);
+        float pr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pr[i] = ex2(x[i] - mn);
+        l_[ht] = l_[ht] * alpha + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+        m_[ht] = mn;
+        // accumulators of lane (g, t) hold head t (+4 ht): its alpha lives in lane 8t
+        const float a_acc = __shfl_sync(0xffffffffu, alpha, 8 * t);
+        if (!__all_sync(0xffffffffu, a_acc == 1.f)) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            acc[ht][i][0] *= a_acc; acc[ht][i][1] *= a_acc; acc[ht][i][2] *= a_acc; acc[ht][i][3] *= a_acc;
+          }
+        }
+        // B operand of the V product: column (head g>>1, parity g&1), rows (token, parity)
+        const uint32_t H0 = pack_half2(pr[0], pr[1]), H1 = pack_half2(pr[2], pr[3]);
+        bb[ht][0] = prmt(H0, 0u, sel_lo);
+        bb[ht][1] = prmt(H0, 0u, sel_hi);
+        bb[ht][2] = prmt(H1, 0u, sel_lo);
+        bb[ht][3] = prmt(H1, 0u, sel_hi);
+      }
+    };
+    // a8 for one block: O'[pair][(head, parity)] += V'[pair][(token, e)] . P'
+    auto values = [&](const uint32_t (&vr)[4][8], const uint32_t (&bb)[NT][4]) {
+#pragma unroll
+      for (int ht = 0; ht < NT; ++ht)
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          mma16816(acc[ht][mt], vr[0][mt], vr[0][4 + mt], vr[1][mt], vr[1][4 + mt], bb[ht][0], bb[ht][1]);
+          mma16816(acc[ht][mt], vr[2][mt], vr[2][4 + mt], vr[3][mt], vr[3][4 + mt], bb[ht][2], bb[ht][3]);
+        }
+    };
+
+    // -------- compressed blocks [lo, min(hi, nbc))
+    const int bend = min(hi, nbc);
+    for (int b = lo; b < bend; ++b, ++cseq) {
+      const int s = cseq % kWNst;
+      const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes);
+      mbar_wait_u32(bar0 + 8 * s, (uint32_t)(cseq / kWNst) & 1u);
+      const int nvalid = min(16, cn.nc - b * 16);
+      build_pairs<NK>(st + p.off_kval, ypk, p.kpk >> 3, p.swk, lane);
+      build_pairs<NV>(st + p.off_vval, ypv, p.kpv >> 3, p.swv, lane);
+      // K bitmap word t of tokens g, g + 8; V half-word g of tokens 2t, 2t+1, 8+2t, 9+2t
+      const uint32_t kw0 = g < nvalid ? lds32(st + 16 * g + 4 * t) : 0u;
+      const uint32_t kw1 = g + 8 < nvalid ? lds32(st + 16 * (g + 8) + 4 * t) : 0u;
+      const int tk[4] = {2 * t, 2 * t + 1, 8 + 2 * t, 9 + 2 * t};
+      uint32_t hw[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        hw[x] = tk[x] < nvalid ? (lds32(st + p.off_vbm + 16 * tk[x] + 4 * (g >> 1)) >> (16 * (g & 1))) & 0xFFFFu : 0u;
+      __syncwarp();
+      // the stage is fully read: refill it with block cseq + kWNst (WAR vs the TMA write)
+      if (!pdone) {
+        if (lane == 0) {
+          fence_proxy_async_smem();
+          p_issue();
+        }
+        ++pseq;
+        ++pb;
+        p_advance();
+      }
+      // exclusive prefixes: K over the 4 words of a token (lanes t), V over the 8 half-words
+      // (lanes g, stride 4), 4 tokens in 4 bytes
+      const uint32_t pk = __popc(kw0) | (__popc(kw1) << 16);
+      uint32_t ik = pk;
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
+        if (t >= o) ik += y;
+      }
+      const uint32_t ek = ik - pk;
+      const uint32_t pv = __popc(hw[0]) | (__popc(hw[1]) << 8) | (__popc(hw[2]) << 16) | (__popc(hw[3]) << 24);
+      uint32_t iv = pv;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, iv, 4 * o);
+        if (g >= o) iv += y;
+      }
+      const uint32_t ev = iv - pv;
+      const bool valid[4] = {tk[0] < nvalid, tk[1] < nvalid, tk[2] < nvalid, tk[3] < nvalid};
+      uint32_t bb[NT][4];
+      {
+        uint32_t kr[2][16];
+        gather16(kw0, ypk + 4u * ((uint32_t)(g * p.swk) + (ek & 0xFFFFu)), kr[0]);
+        gather16(kw1, ypk + 4u * ((uint32_t)((g + 8) * p.swk) + (ek >> 16)), kr[1]);
+        scores(kr, valid, bb);
+      }
+      {
+        uint32_t vr[4][8];
+#pragma unroll
+        for (int x = 0; x < 4; x += 2)
+          gather8x2(hw[x] | (hw[x + 1] << 16), ypv + 4u * ((uint32_t)(tk[x] * p.swv) + ((ev >> (8 * x)) & 0xFFu)),
+                    ypv + 4u * ((uint32_t)(tk[x + 1] * p.swv) + ((ev >> (8 * x + 8)) & 0xFFu)), vr[x], vr[x + 1]);
+        values(vr, bb);
+      }
+    }
+
+    // -------- window blocks [max(lo, nbc), hi): dense ring rows (a6)
+    const int wlo = max(lo, nbc);
+    if (wlo < hi) {
+      if (p.fuse) {
+        if (lane == 0) wait_ready(p.ready + u);
+        __syncwarp();
+      }
+      const int first = c.W > 0 ? cn.nc % c.W : 0;
+      const uint16_t* wk = c.win[0] + (size_t)u * c.W * kD;
+      const uint16_t* wv = c.win[1] + (size_t)u * c.W * kD;
+      for (int x = wlo; x < hi; ++x) {
+        const int row0 = (x - nbc) * 16;
+        auto ok = [&](int r) {  // ring slot row0 + r holds a window token
+          const int slot = row0 + r;
+          int age = slot - first;
+          if (age < 0) age += c.W;
+          return slot < c.W && age < cn.nw;
+        };
+        if (!__any_sync(0xffffffffu, ok(lane & 15))) continue;
+        const int tk[4] = {2 * t, 2 * t + 1, 8 + 2 * t, 9 + 2 * t};
+        bool valid[4];
+#pragma unroll
+        for (int xx = 0; xx < 4; ++xx) valid[xx] = ok(tk[xx]);
+        uint32_t bb[NT][4];
+        {
+        uint32_t kr[2][16];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int tok = g + 8 * nt;
+          if (ok(tok)) {
+            const uint4* pp = reinterpret_cast<const uint4*>(wk + (size_t)(row0 + tok) * kD + 32 * t);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 a = __ldcg(pp + i);
+              kr[nt][4 * i] = a.x; kr[nt][4 * i + 1] = a.y; kr[nt][4 * i + 2] = a.z; kr[nt][4 * i + 3] = a.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) kr[nt][i] = 0u;
+          }
+        }
+        scores(kr, valid, bb);
+        }
+        uint32_t vr[4][8];
+#pragma unroll
+        for (int xx = 0; xx < 4; ++xx) {
+          if (valid[xx]) {
+            const uint4* pp = reinterpret_cast<const uint4*>(wv + (size_t)(row0 + tk[xx]) * kD + 16 * g);
+            const uint4 a = __ldcg(pp), b2 = __ldcg(pp + 1);
+            vr[xx][0] = a.x; vr[xx][1] = a.y; vr[xx][2] = a.z; vr[xx][3] = a.w;
+            vr[xx][4] = b2.x; vr[xx][5] = b2.y; vr[xx][6] = b2.z; vr[xx][7] = b2.w;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vr[xx][i] = 0u;
+          }
+        }
+        values(vr, bb);
+      }
+    }
+
+    // -------- segment partial (slot P + u): m, l (log2 domain), o unnormalised
+    const size_t slot = (size_t)P + u;
+#pragma unroll
+    for (int ht = 0; ht < NT; ++ht) {
+      float l = l_[ht];
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      const int hm = h0 + 4 * ht;  // head of this lane's score rows
+      if ((g & 1) == 0 && t == 0 && hm < p.G)
+        *reinterpret_cast<float2*>(p.ws_ml + (slot * p.G + hm) * 2) = make_float2(m_[ht], l);
+      const int ho = t + 4 * ht;   // head of this lane's accumulators
+      if (ho < p.G) {
+        float4* o = reinterpret_cast<float4*>(p.ws_o + (slot * p.G + ho) * kD + 16 * g);
+        o[0] = make_float4(acc[ht][0][0], acc[ht][0][1], acc[ht][1][0], acc[ht][1][1]);
+        o[1] = make_float4(acc[ht][2][0], acc[ht][2][1], acc[ht][3][0], acc[ht][3][1]);
+        o[2] = make_float4(acc[ht][0][2], acc[ht][0][3], acc[ht][1][2], acc[ht][1][3]);
+        o[3] = make_float4(acc[ht][2][2], acc[ht][2][3], acc[ht][3][2], acc[ht][3][3]);
+      }
+    }
+  }
+}
+
+// Ragged caches: cost prefix over the units from the device counters (one CTA).
+__global__ void mstf_cost_prefix_kernel(const WParams p) {
+  pdl_launch_dependents();
+  pdl_wait();
+  __shared__ int s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_w[32];
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < p.c.U; base += blockDim.x) {
+    const int u = base + threadIdx.x;
+    const int v = u < p.c.U ? cost_of(p, counters_of(p, u).nc) : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int x = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      s_w[lane] = x;
+    }
+    __syncthreads();
+    const int before = s_carry + (warp ? s_w[warp - 1] : 0);
+    if (u < p.c.U) p.pref[u] = before + incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = before + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.pref[p.c.U] = s_carry;
+}
+
+// a9: one CTA per unit merges the unit's partial slots (the workers overlapping its cost
+// range). G warps (one per head) x S sub-warps splitting the slots when units are few.
+// In a fused step it then writes the unit's post-append counters and clears its ready flag.
+template <bool SUB>
+__global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p) {
+  pdl_launch_dependents();
+  pdl_wait();  // partials and the plan header come from the attention kernel just before
+  extern __shared__ __align__(16) float s_comb[];
+  const int G = p.G;
+  const int u = blockIdx.x, wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = SUB ? wi % G : wi, sub = SUB ? wi / G : 0, Sn = SUB ? blockDim.x / (32 * G) : 1;
+  const long long S = p.hdr[0];
+  const int cpu = p.hdr[1];
+  const int us = cpu ? u * cpu : p.pref[u], ue = cpu ? (u + 1) * cpu : p.pref[u + 1];
+  // workers overlapping [us, ue): first = owner of us, last = owner of ue - 1
+  const int wf = (int)(((long long)(us + 1) * p.np - 1) / S), wl = (int)(((long long)ue * p.np - 1) / S);
+  const int np_ = wl - wf + 1;
+  const int i_lo = np_ * sub / Sn, i_hi = np_ * (sub + 1) / Sn;
+  float m_max = -INFINITY, l_sum = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (h < G) {
+    constexpr int kB = 16;  // slots per batch: all their loads are issued before any math
+    for (int i0 = i_lo; i0 < i_hi; i0 += kB) {
+      const int cnt = min(kB, i_hi - i0);
+      float2 ml = make_float2(-INFINITY, 0.f);
+      if (lane < cnt) ml = *reinterpret_cast<const float2*>(p.ws_ml + ((size_t)(wf + i0 + lane + u) * G + h) * 2);
+      float4 v[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i)
+        v[i] = i < cnt ? *(reinterpret_cast<const float4*>(p.ws_o + ((size_t)(wf + i0 + i + u) * G + h) * kD) + lane)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      float mb = ml.x;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+      const float mn = fmaxf(m_max, mb);
+      if (mn == -INFINITY) continue;
+      const float a = exp2f(m_max - mn);
+      const float wgt = ml.x == -INFINITY ? 0.f : exp2f(ml.x - mn);
+      float lb = wgt * ml.y;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) lb += __shfl_xor_sync(0xffffffffu, lb, o);
+      l_sum = l_sum * a + lb;
+      acc.x *= a; acc.y *= a; acc.z *= a; acc.w *= a;
+      m_max = mn;
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const float wi2 = __shfl_sync(0xffffffffu, wgt, i);
+        if (wi2 != 0.f) {  // an empty segment's o slot is never written
+          acc.x += wi2 * v[i].x; acc.y += wi2 * v[i].y; acc.z += wi2 * v[i].z; acc.w += wi2 * v[i].w;
+        }
+      }
+    }
+  }
+  if (SUB && Sn > 1) {
+    float* s_acc = s_comb;
+    float2* s_ml = reinterpret_cast<float2*>(s_comb + (Sn - 1) * G * kD);
+    if (sub > 0 && h < G) {
+      *reinterpret_cast<float4*>(s_acc + ((sub - 1) * G + h) * kD + 4 * lane) = acc;
+      if (lane == 0) s_ml[(sub - 1) * G + h] = make_float2(m_max, l_sum);
+    }
+    __syncthreads();
+    if (sub == 0 && h < G) {
+      for (int j = 0; j < Sn - 1; ++j) {
+        const float2 o = s_ml[j * G + h];
+        const float mn = fmaxf(m_max, o.x);
+        if (mn == -INFINITY) continue;
+        const float a = exp2f(m_max - mn), b2 = exp2f(o.x - mn);
+        const float4 x = *reinterpret_cast<const float4*>(s_acc + (j * G + h) * kD + 4 * lane);
+        acc.x = acc.x * a + x.x * b2; acc.y = acc.y * a + x.y * b2;
+        acc.z = acc.z * a + x.z * b2; acc.w = acc.w * a + x.w * b2;
+        l_sum = l_sum * a + o.y * b2;
+        m_max = mn;
+      }
+    }
+  }
+  if (sub == 0 && h < G) {
+    const size_t oi = ((size_t)u * G + h) * kD + 4 * lane;
+    if (p.part_ml) {  // sequence-split shard: unnormalised partials (log2 domain)
+      *reinterpret_cast<float4*>(p.part_o + oi) = acc;
+      if (lane == 0) *reinterpret_cast<float2*>(p.part_ml + ((size_t)u * G + h) * 2) = make_float2(m_max, l_sum);
+    } else {
+      const float inv = 1.f / l_sum;
+      if (p.out_f16) {
+        __half2* po = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.out) + oi);
+        po[0] = __floats2half2_rn(acc.x * inv, acc.y * inv);
+        po[1] = __floats2half2_rn(acc.z * inv, acc.w * inv);
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oi) =
+            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      }
+    }
+  }
+  if (p.fuse && threadIdx.x == 0) {  // a4 bookkeeping of the fused step (after every reader)
+    const int nc = p.c.n_comp[u], nw = p.c.n_win[u];
+    if (p.c.W == 0 || nw == p.c.W) p.c.n_comp[u] = nc + 1; else p.c.n_win[u] = nw + 1;
+    p.ready[u] = 0;
+  }
+}
+
+template <int NK, int NV>
+void* pick_kernel(bool g8) {
+  return g8 ? (void*)mstf_attn_warp_kernel<NK, NV, true> : (void*)mstf_attn_warp_kernel<NK, NV, false>;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+static size_t r256(size_t b) { return (b + 255) / 256 * 256; }
+
+size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count) {
+  const size_t slots = (size_t)sm_count * kWMaxWarps + U + 1;
+  return r256(kWHdrInts * sizeof(int)) + r256((size_t)U * sizeof(int)) + r256((size_t)(U + 1) * sizeof(int)) +
+         r256(slots * G * 2 * sizeof(float)) + slots * G * kD * sizeof(float);
+}
+
+bool warp_kernel_supported(int32_t G) { return G >= 1 && G <= 8; }
+
+static int pair_sw(int kp) { return kp + 4; }  // words per token: Y[0..kp], rows 16-byte aligned
+
+int warp_region_bytes(int32_t kpk, int32_t kpv, int* stage_bytes) {
+  const int st = 16 * (16 + 2 * kpk) + 16 * (16 + 2 * kpv);
+  if (stage_bytes) *stage_bytes = st;
+  const int pairs = 64 * pair_sw(kpk) + 64 * pair_sw(kpv);
+  return (kWNst * st + pairs + 8 * kWNst + 127) / 128 * 128;
+}
+
+WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t sm_count) {
+  WarpPlan pl;
+  const int wb = warp_region_bytes(kpk, kpv, nullptr);
+  int wmax = (int)((227 * 1024) / wb);
+  const int wcap = G > 4 ? kWMaxWarps / 2 : kWMaxWarps;
+  if (wmax > wcap) wmax = wcap;
+  if (wmax < 1) wmax = 1;
+  // >= ~4 cost units per worker (each worker pays a segment prologue and writes a partial)
+  const int64_t qmin = 4;
+  int64_t workers = (total_cost + qmin - 1) / qmin;
+  if (workers < 1) workers = 1;
+  int grid = sm_count, wpc = wmax;
+  if (workers < (int64_t)grid * wmax) {
+    wpc = (int)std::max<int64_t>(1, (workers + grid - 1) / grid);
+    if (wpc > wmax) wpc = wmax;
+    if ((int64_t)grid * wpc > workers) grid = (int)std::max<int64_t>(1, (workers + wpc - 1) / wpc);
+  }
+  if (const char* e = std::getenv("MSTF_WPC")) {  // dev A/B: warps per CTA
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= wmax) wpc = v;
+  }
+  pl.grid = grid;
+  pl.wpc = wpc;
+  pl.warp_bytes = wb;
+  pl.smem = wpc * wb;
+  return pl;
+}
+
+cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int32_t G, int32_t uniform, int32_t fuse,
+                                  const uint16_t* q, float scale, const uint16_t* k_new, const uint16_t* v_new,
+                                  void* out, int32_t out_f16, float* part_ml, float* part_o, void* ws,
+                                  int32_t sm_count, cudaStream_t s) {
+  WParams p;
+  p.c = c;
+  p.q = q;
+  p.G = G;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.np = plan.grid * plan.wpc;
+  p.wpc = plan.wpc;
+  sk_cost_params(&p.cs, &p.cw);
+  p.uniform = uniform;
+  p.fuse = fuse;
+  p.kpk = c.kpad[0];
+  p.kpv = c.kpad[1];
+  p.stage_bytes = 0;
+  p.warp_bytes = warp_region_bytes(p.kpk, p.kpv, &p.stage_bytes);
+  p.off_kval = 256;
+  p.off_vbm = p.off_kval + 32 * p.kpk;
+  p.off_vval = p.off_vbm + 256;
+  p.swk = pair_sw(p.kpk);
+  p.swv = pair_sw(p.kpv);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  p.hdr = reinterpret_cast<int*>(w);
+  w += r256(kWHdrInts * sizeof(int));
+  p.ready = reinterpret_cast<int*>(w);
+  w += r256((size_t)c.U * sizeof(int));
+  p.pref = reinterpret_cast<int*>(w);
+  w += r256((size_t)(c.U + 1) * sizeof(int));
+  const size_t slots = (size_t)sm_count * kWMaxWarps + c.U + 1;
+  p.ws_ml = reinterpret_cast<float*>(w);
+  w += r256(slots * G * 2 * sizeof(float));
+  p.ws_o = reinterpret_cast<float*>(w);
+  p.k_new = k_new;
+  p.v_new = v_new;
+  p.out = out;
+  p.out_f16 = out_f16;
+  p.part_ml = part_ml;
+  p.part_o = part_o;
+
+  cudaError_t e;
+  if (!uniform) {
+    e = launch_pdl(mstf_cost_prefix_kernel, dim3(1), dim3(1024), 0, s, p);
+    if (e != cudaSuccess) return e;
+  }
+  const bool g8 = G > 4;
+  void* kern = nullptr;
+  const int nk = c.kpad[0] / 8, nv = c.kpad[1] / 8;
+  if (nk == nv && nk == 5) kern = pick_kernel<5, 5>(g8);
+  else if (nk == nv && nk == 8) kern = pick_kernel<8, 8>(g8);
+  else if (nk == nv && nk == 4) kern = pick_kernel<4, 4>(g8);
+  else if (nk == nv && nk == 2) kern = pick_kernel<2, 2>(g8);
+  else kern = pick_kernel<0, 0>(g8);
+  void (*kf)(WParams) = reinterpret_cast<void (*)(WParams)>(kern);
+  e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(kf, dim3(plan.grid), dim3(32 * plan.wpc), (size_t)plan.smem, s, p);
+  if (e != cudaSuccess) return e;
+  // combine: sub-warps per head when a unit has many partial slots (few units)
+  const int64_t slots_per_unit = ((int64_t)p.np + c.U - 1) / c.U + 2;
+  int sub = (int)((slots_per_unit + 15) / 16);
+  sub = std::max(1, std::min(std::min(sub, 4), 512 / (32 * G)));
+  if (sub == 1) return launch_pdl(mstf_warp_combine_kernel<false>, dim3(c.U), dim3(32 * G), 0, s, p);
+  const size_t csmem = (size_t)(sub - 1) * G * (kD * sizeof(float) + sizeof(float2));
+  return launch_pdl(mstf_warp_combine_kernel<true>, dim3(c.U), dim3(32 * G * sub), csmem, s, p);
+}
+
+}  // namespace mstf

@@ -111,6 +111,25 @@ cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const i
                                    int32_t G, int32_t t_max, int32_t splits, const uint16_t* q, float scale,
                                    void* out, int32_t out_f16, void* ws, cudaStream_t s);
 
+// r2 attention (attn_warp.cu): one self-contained warp per stream-K worker, TMA-staged blocks,
+// device-side partition from the device counters (CUDA-graph replayable), optional fused append.
+struct WarpPlan {
+  int32_t grid;        // CTAs (<= SMs, one per SM)
+  int32_t wpc;         // warps (workers) per CTA
+  int32_t warp_bytes;  // shared memory per warp
+  int32_t smem;        // dynamic shared memory per CTA
+};
+bool warp_kernel_supported(int32_t G);
+size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count);
+int warp_region_bytes(int32_t kpk, int32_t kpv, int* stage_bytes);
+WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t sm_count);
+// uniform: every unit has the same counters (fuse requires it). fuse: k_new / v_new are appended
+// inside the launch (the counters are then advanced by the combine kernel).
+cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int32_t G, int32_t uniform, int32_t fuse,
+                                  const uint16_t* q, float scale, const uint16_t* k_new, const uint16_t* v_new,
+                                  void* out, int32_t out_f16, float* part_ml, float* part_o, void* ws,
+                                  int32_t sm_count, cudaStream_t s);
+
 // dev: copy the per-CTA timeline recorded when MSTF_TRACE is set (n = 3 * CTAs words)
 cudaError_t copy_trace(void* host, int n);
 

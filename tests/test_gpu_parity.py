@@ -203,7 +203,6 @@ def test_attention_ragged_units(M):
     assert check_attention(M, gc, oc, 2, 16, 4, seed=77) <= TOL
 
 
-@pytest.mark.parametrize("sched", ["split", "stream-k"])
 @pytest.mark.parametrize("case", [
     # (batch, hq, hkv, T, keep, W, lengths per unit or None)
     (16, 32, 8, 600, 39, 32, None),                                   # uniform: stream-K without prefix
@@ -213,12 +212,11 @@ def test_attention_ragged_units(M):
     (2, 8, 2, 1000, 16, 16, None),                                    # kpad 16 kernel
     (4, 16, 4, 700, 64, 64, [700, 5, 64, 333] * 4),                   # kpad 64 (50% sparsity)
 ])
-def test_attention_schedules(M, monkeypatch, sched, case):
-    """Both work schedules of the register-staged kernel (split grid; stream-K with units
-    concatenated and CTA ranges crossing unit boundaries) against the oracle."""
+def test_attention_schedules(M, case):
+    """The stream-K schedule (units' blocks concatenated, worker ranges crossing unit
+    boundaries; ragged caches through the device-side cost prefix) at several k_pad values,
+    against the oracle."""
     U_b, hq, hkv, T, keep, W, lengths = case
-    if sched == "split":
-        monkeypatch.setenv("MSTF_SCHED", "split")
     gc, oc = make(M, U_b, hq, hkv, T, keep, keep, W, lengths=lengths, seed=T + keep)
     assert check_attention(M, gc, oc, U_b, hq, hkv, seed=T) <= TOL
 
@@ -314,8 +312,9 @@ def test_decode_step_equals_append_then_attention(M, case):
         q = synth.fp16_np((U, G, 128), synth.seed_for(500 + i, 2))
         qd = torch.from_numpy(q.view(np.int16)).cuda().view(torch.float16)
         kn, vn = Kd[:, T + i].contiguous(), Vd[:, T + i].contiguous()
-        fused = lengths is None and kk == kv and O.k_pad_of(kk) in (16, 32, 40, 64)
-        assert cf.decode_step_kernel_count() == (2 if fused else 3)
+        fused = lengths is None   # uniform cache: append inside the attention launch
+        # fused: attention + combine; ragged: append + cost prefix + attention + combine
+        assert cf.decode_step_kernel_count() == (2 if fused else 4)
         of = cf.decode_step(kn, vn, qd, scale)
         cs.append_token(kn, vn)
         os_ = cs.sparse_decode_attention(qd, scale)
