@@ -43,10 +43,37 @@ WORKLOADS = {
     "C3": dict(desc="Llama-2-7B shape MHA decode, 32 heads, d=128, 32K context, batch 1, 70% sparsity",
                batch=1, hq=32, hkv=32, T=32768, sk=0.7, sv=0.7),
     "C4": dict(desc="Llama-3-8B shape, 128K context, batch 8, 70% sparsity", batch=8, hq=32, hkv=8, T=131072,
-               sk=0.7, sv=0.7, layers=4),
+               sk=0.7, sv=0.7),
     "C5": dict(desc="Llama-3-8B shape, 16K context, batch 64 per GPU, 70% sparsity", batch=64, hq=32, hkv=8,
-               T=16384, sk=0.7, sv=0.7, layers=8),
+               T=16384, sk=0.7, sv=0.7),
 }
+DEFAULT_WORKLOAD = "C4"   # the largest single-GPU configuration of BASELINE.json (128K context)
+SPEC_HBM_GBS = 8000.0     # nominal B200 HBM3e (DGX figure; B200_PROFILING.md: 7.7 HGX / 8 DGX)
+
+
+def unit_string(L):
+    return f"tokens/s (attention-only decode, {L} layers)"
+
+
+def config_of(args, cfg, world, L, extra=None):
+    """The config object both arms print (the reference arm copies ours)."""
+    B = cfg["batch"]
+    c = {"workload": args.workload, "desc": cfg["desc"], "batch_per_gpu": B, "global_batch": B * world,
+         "num_q_heads": cfg["hq"], "num_kv_heads": cfg["hkv"], "head_dim": 128, "context": cfg["T"],
+         "keep_k": keep_of(cfg["sk"]), "keep_v": keep_of(cfg["sv"]), "window": W_WINDOW, "layers": L}
+    if extra:
+        c.update(extra)
+    return c
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def keep_of(s, d=128):
@@ -201,7 +228,7 @@ def oracle_sample(cfg, seconds=10.0, max_units=64):
     B, hq, hkv, T = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["T"]
     U, G, d = B * hkv, hq // hkv, 128
     kk, kv = keep_of(cfg["sk"]), keep_of(cfg["sv"])
-    layers = cfg.get("layers", LAYERS)
+    layers = LAYERS
     per_unit = []
     with threadpool_limits(limits=1):
         t_budget = time.perf_counter() + seconds
@@ -220,8 +247,105 @@ def oracle_sample(cfg, seconds=10.0, max_units=64):
     t_unit = statistics.mean(per_unit)
     step_s = t_unit * U * layers
     desc = (f"{len(per_unit)} units of layer 0 (append + fp64 Alg.1 over {T} tokens each), "
-            f"{t_unit * 1e3:.1f} ms/unit, extrapolated x{U} units x{layers} layers")
-    return B / step_s, desc, 1
+            f"{t_unit * 1e3:.1f} ms/unit, extrapolated x{U} units x{layers} layers; "
+            f"host CPU: {cpu_model()}, {os.cpu_count()} logical cores, 1 thread used")
+    return B / step_s, desc, 1, t_unit, len(per_unit)
+
+
+# ----------------------------------------------------------------------------- dense baselines
+def dense_baselines(M, B, hq, hkv, d, Tn, t_alloc, scale, dense_k, dense_v, q0, dev, reps=3):
+    """Dense-KV decode attention over the same shapes (fp16 KV of `len(dense_k)` layers, rotated
+    so the working set exceeds L2): the repo's own dense kernel, torch SDPA, FlashAttention-2
+    decode (flash_attn_with_kvcache, split-KV: auto and explicit num_splits) and FlashInfer's
+    batch decode on a paged cache (page 16 and 64, CUDA-core and tensor-core variants, planned
+    outside the timing). Returns {name: us per layer} and the fastest."""
+    import torch
+    U, G = B * hkv, hq // hkv
+    L = len(dense_k)
+    res, notes = {}, {}
+
+    def time_fn(fn):
+        for l in range(L):
+            fn(l)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            for l in range(L):
+                fn(l)
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) * 1e3 / (reps * L)
+
+    lengths = torch.full((U,), Tn, dtype=torch.int32, device=dev)
+    o16 = torch.empty(U, G, d, dtype=torch.float16, device=dev)
+    try:
+        da = M.DenseAttention(U, G, d, t_alloc, device=dev)
+        res["own_dense_kernel"] = time_fn(lambda l: da(dense_k[l], dense_v[l], lengths, q0, scale, out=o16))
+    except Exception as ex:  # noqa: BLE001
+        notes["own_dense_kernel"] = str(ex)[:120]
+    import torch.nn.functional as F
+    qs = q0.view(B, hq, 1, d)
+    k4 = [k.view(B, hkv, t_alloc, d)[:, :, :Tn] for k in dense_k]
+    v4 = [v.view(B, hkv, t_alloc, d)[:, :, :Tn] for v in dense_v]
+    try:
+        res["torch_sdpa"] = time_fn(lambda l: F.scaled_dot_product_attention(qs, k4[l], v4[l], scale=scale,
+                                                                              enable_gqa=True))
+    except Exception as ex:  # noqa: BLE001
+        notes["torch_sdpa"] = str(ex)[:120]
+    # FlashAttention-2 decode: [B, T, Hkv, d] cache (a layout copy, made outside the timing)
+    try:
+        from flash_attn import flash_attn_with_kvcache
+        kf = [x.transpose(1, 2).contiguous() for x in k4]
+        vf = [x.transpose(1, 2).contiguous() for x in v4]
+        qf = q0.view(B, 1, hq, d)
+        best = None
+        for ns in (0, 1, 2, 4, 8, 16, 32):
+            us = time_fn(lambda l: flash_attn_with_kvcache(qf, kf[l], vf[l], softmax_scale=scale, num_splits=ns))
+            if best is None or us < best[0]:
+                best = (us, ns)
+        res["flash_attn_kvcache"] = best[0]
+        notes["flash_attn_kvcache"] = f"num_splits={best[1]} (best of 0=auto,1,2,4,8,16,32)"
+        del kf, vf
+    except Exception as ex:  # noqa: BLE001
+        notes["flash_attn_kvcache"] = str(ex)[:160]
+    # FlashInfer batch decode on a paged cache [pages, 2, page, Hkv, d] (NHD)
+    try:
+        import flashinfer
+        ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        best = None
+        for page in (16, 64):
+            npg = (Tn + page - 1) // page
+            kv = []
+            for l in range(L):
+                x = torch.zeros(B * npg, 2, page, hkv, d, dtype=torch.float16, device=dev)
+                kb = k4[l].transpose(1, 2)  # [B, Tn, Hkv, d]
+                vb = v4[l].transpose(1, 2)
+                xs = x.view(B, npg, 2, page, hkv, d)
+                full = (Tn // page) * page
+                xs[:, :Tn // page, 0] = kb[:, :full].reshape(B, Tn // page, page, hkv, d)
+                xs[:, :Tn // page, 1] = vb[:, :full].reshape(B, Tn // page, page, hkv, d)
+                if Tn % page:
+                    xs[:, Tn // page, 0, :Tn % page] = kb[:, full:]
+                    xs[:, Tn // page, 1, :Tn % page] = vb[:, full:]
+                kv.append(x)
+            indptr = torch.arange(0, B + 1, dtype=torch.int32, device=dev) * npg
+            idx = torch.arange(B * npg, dtype=torch.int32, device=dev)
+            last = torch.full((B,), Tn - (npg - 1) * page, dtype=torch.int32, device=dev)
+            for tc in (False, True):
+                w = flashinfer.BatchDecodeWithPagedKVCacheWrapper(ws, "NHD", use_tensor_cores=tc)
+                w.plan(indptr, idx, last, hq, hkv, d, page, q_data_type=torch.float16, kv_data_type=torch.float16,
+                       sm_scale=scale)
+                q2 = q0.view(B, hq, d)
+                us = time_fn(lambda l: w.run(q2, kv[l]))
+                if best is None or us < best[0]:
+                    best = (us, page, tc)
+            del kv
+        res["flashinfer_batch_decode"] = best[0]
+        notes["flashinfer_batch_decode"] = f"page_size={best[1]} use_tensor_cores={best[2]} (best of 16/64 x CUDA/tensor cores)"
+    except Exception as ex:  # noqa: BLE001
+        notes["flashinfer_batch_decode"] = str(ex)[:160]
+    return res, notes
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -243,19 +367,24 @@ def run_ours(args, cfg, rank, world, local_rank):
     B, hq, hkv, T = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["T"]
     U, G, d = B * hkv, hq // hkv, 128
     kk, kv = keep_of(cfg["sk"]), keep_of(cfg["sv"])
-    L = cfg.get("layers", LAYERS) if args.layers is None else args.layers
+    L = LAYERS if args.layers is None else args.layers
     K_steps, W_steps = args.steps, args.warmup
-    # warm-up, the headline timed pass (no events between kernels, so programmatic dependent
-    # launch can overlap them), and a second timed pass with events around every attention
-    # call for the roofline's per-launch kernel time
-    total_steps = W_steps + 2 * K_steps
+    # warm-up, the headline timed pass (no events between a step's kernels, so programmatic
+    # dependent launch overlaps them), a second pass with events around every layer call (the
+    # roofline's per-launch time), and the end-to-end pass
+    total_steps = W_steps + 2 * K_steps + 8
     T0 = T - 1                       # prefill length; the first decode token makes it T
-    cap = T0 - W_WINDOW + 2 * total_steps + 8
+    cap = T0 - W_WINDOW + total_steps + 8
     scale = 1 / math.sqrt(d)
+    gather = args.gather if args.gather is not None else world > 1
 
-    # ---- caches (one per layer), prefilled from synthetic K/V; dense copies kept for the baseline
-    caches, dense_k, dense_v = [], [], []
-    pf_events = []
+    # ---- L layer caches, each prefilled from synthetic K/V; dense copies of a few layers for the
+    # dense baselines (enough layers that their working set exceeds the 126 MB L2)
+    dense_layers = 0
+    if args.dense:
+        per_layer_dense = U * (T + total_steps) * d * 2 * 2
+        dense_layers = max(2, min(L, -(-3 * 128 * 2**20 // per_layer_dense)))
+    caches, dense_k, dense_v, pf_events = [], [], [], []
     for l in range(L):
         seed = synth.seed_for(2, 10 * l + 1000 * rank)
         Kl = synth.fp16_torch((U, T + total_steps, d), seed, device=dev)
@@ -269,7 +398,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         pf_events.append((e0, e1))
         del Kp, Vp
         caches.append(c)
-        if args.dense:
+        if l < dense_layers:
             dense_k.append(Kl)
             dense_v.append(Vl)
         else:
@@ -291,14 +420,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         vn = x[U * G * d + U * d:].view(U, d)
         return q, kn, vn
 
-    outs = [torch.empty(U, G, d, dtype=torch.float16, device=dev) for _ in range(L)]
-    # --gather: every layer's output is all-gathered in place into the
-    # [B_global][Hq][d] tensor (rank r's slice is its units' [U][G][d]) -- the serving layout.
-    # Off by default: the units are independent, so the measured path has no collective.
-    gather = args.gather and world > 1
+    # outputs: with the a10 gather (default for N > 1) every layer's output is written
+    # straight into this rank's slice of the [B_global][Hq][d] tensor and all-gathered in place
     full = [torch.empty(world * U, G, d, dtype=torch.float16, device=dev) for _ in range(L)] if gather else None
-    if gather:
-        outs = [f[rank * U:(rank + 1) * U] for f in full]
+    outs = [f[rank * U:(rank + 1) * U] for f in full] if gather else \
+        [torch.empty(U, G, d, dtype=torch.float16, device=dev) for _ in range(L)]
     torch.cuda.synchronize()
 
     # per-(slab, layer) input views built once, outside the timed region: at small batch the
@@ -306,13 +432,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     view_cache = {}
     cur_stream = torch.cuda.current_stream()
 
-    def step(slab, ev=None):
+    def step(slab, ev=None, do_gather=gather):
         # one decode step per layer: append (a4) + attention (Alg. 1) in one C-ABI call
-        # (mstf_decode_step: a single fused launch + the split combine for uniform caches)
-        key = slab.data_ptr()
-        vs = view_cache.get(key)
-        if vs is None:
-            vs = view_cache[key] = [views(slab, l) for l in range(L)]
+        # (mstf_decode_step: the append inside the attention launch + the split combine)
+        vs = view_cache[slab.data_ptr()]
         for l in range(L):
             q, kn, vn = vs[l]
             if ev is not None:
@@ -320,10 +443,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             caches[l].decode_step(kn, vn, q, scale, out=outs[l], stream=cur_stream)
             if ev is not None:
                 ev[l][1].record()
-            if gather:
+            if do_gather:
                 dist.all_gather_into_tensor(full[l], outs[l])  # in place: outs[l] is this rank's slice
 
-    # ---- device-timed region
     for s_ in range(total_steps):
         view_cache[gen[s_].data_ptr()] = [views(gen[s_], l) for l in range(L)]
     sampler = ClockSampler(local_rank)
@@ -333,25 +455,40 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # ---- headline: K steps, device-timed; an event at every step boundary gives p10/p50/p90
     sampler.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(K_steps + 1)]
+    sev[0].record()
     for s in range(K_steps):
         step(gen[W_steps + s])
-    e1.record()
+        sev[s + 1].record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = e0.elapsed_time(e1) / K_steps
-    # second timed pass: same step, CUDA events on the launching stream around each attention call
+    ms = sev[0].elapsed_time(sev[K_steps]) / K_steps
+    step_ms = sorted(sev[i].elapsed_time(sev[i + 1]) for i in range(K_steps))
+    pct = lambda q_: step_ms[min(len(step_ms) - 1, int(round(q_ * (len(step_ms) - 1))))]
+    # second timed pass: same step, CUDA events on the launching stream around each layer's call
     for s in range(K_steps):
-        step(gen[W_steps + K_steps + s], attn_ev[s])
+        step(gen[W_steps + K_steps + s], attn_ev[s], do_gather=False)
     torch.cuda.synchronize()
     clocks = sampler.stop()
     if world > 1:
         dist.barrier()
     attn_ms = [attn_ev[s][l][0].elapsed_time(attn_ev[s][l][1]) for s in range(K_steps) for l in range(L)]
     attn_us = statistics.mean(attn_ms) * 1e3
+    # a10 alone: the L in-place all-gathers of one step, device-timed
+    gather_us = None
+    if gather:
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        g0.record()
+        for _ in range(3):
+            for l in range(L):
+                dist.all_gather_into_tensor(full[l], outs[l])
+        g1.record()
+        torch.cuda.synchronize()
+        gather_us = g0.elapsed_time(g1) * 1e3 / (3 * L)
     nc, nw = caches[0].counts()
     n_comp, n_win = nc[0], nw[0]
 
@@ -359,8 +496,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # Every step copies its inputs (q, k_new, v_new of all layers) host -> device and reads its
     # result (the last layer's output) back to the host. The copy of step s+1 runs on a copy
     # stream while step s computes (double-buffered device inputs); one sync at the end.
-    e2e_steps = min(K_steps, cap - (n_comp + 1))  # the caches' remaining headroom
-    e2e_steps = max(1, min(e2e_steps, 8))
+    e2e_steps = max(1, min(K_steps, 8, cap - (n_comp + 1)))
     host_in = torch.empty((e2e_steps, L, per_layer), dtype=torch.float16, pin_memory=True)
     host_in.copy_(gen[W_steps:W_steps + e2e_steps].cpu())  # same inputs as the headline pass
     host_out = torch.empty((e2e_steps, U, G, d), dtype=torch.float16, pin_memory=True)
@@ -399,52 +535,49 @@ def run_ours(args, cfg, rank, world, local_rank):
     e2e_ms = f0.elapsed_time(f1) / e2e_steps
     assert torch.isfinite(host_out.float()).all()
 
-    # ---- dense-KV baselines (same shapes, dense fp16 KV of all L layers)
+    # ---- read-only HBM peak (the denominator a pure streaming read reaches on this GPU)
+    read_gbs = None
+    try:
+        buf = torch.empty(4 << 30, dtype=torch.uint8, device=dev)
+        sink = torch.zeros(1, dtype=torch.int32, device=dev)
+        for _ in range(2):
+            M.dev_read_bandwidth(buf, sink)
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        for _ in range(5):
+            M.dev_read_bandwidth(buf, sink)
+        r1.record()
+        torch.cuda.synchronize()
+        read_gbs = buf.numel() * 5 / (r0.elapsed_time(r1) * 1e-3) / 1e9
+        del buf
+    except Exception:  # noqa: BLE001
+        read_gbs = None
+
+    # ---- dense-KV baselines (same shapes): the fastest of several implementations
     dense = {}
-    if args.dense:
-        lengths = torch.full((U,), n_comp + n_win, dtype=torch.int32, device=dev)
+    if args.dense and dense_k:
         Tn = n_comp + n_win
-        da = M.DenseAttention(U, G, d, T + total_steps, device=dev)
         q0 = views(gen[0], 0)[0]
-        o32 = torch.empty(U, G, d, dtype=torch.float16, device=dev)
-
-        def time_dense(fn, reps=3):
-            for l in range(L):
-                fn(l)
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            for _ in range(reps):
-                for l in range(L):
-                    fn(l)
-            b.record()
-            torch.cuda.synchronize()
-            return a.elapsed_time(b) * 1e3 / (reps * L)
-
-        dense["own_kernel_us_per_layer"] = time_dense(
-            lambda l: da(dense_k[l], dense_v[l], lengths, q0, scale, out=o32))
-        try:
-            import torch.nn.functional as F
-            qs = q0.view(B, hq, 1, d)
-
-            def sdpa(l):
-                k4 = dense_k[l].view(B, hkv, T + total_steps, d)[:, :, :Tn]
-                v4 = dense_v[l].view(B, hkv, T + total_steps, d)[:, :, :Tn]
-                return F.scaled_dot_product_attention(qs, k4, v4, scale=scale, enable_gqa=True)
-            dense["torch_sdpa_us_per_layer"] = time_dense(sdpa)
-        except Exception as ex:  # noqa: BLE001
-            dense["torch_sdpa_error"] = str(ex)[:120]
-        best = min(v for k_, v in dense.items() if k_.endswith("_us_per_layer"))
-        dense["best_dense_us_per_layer"] = best
-        dense["dense_bytes_per_layer"] = U * (Tn * 4 * d + 2 * G * d * 2)
-        dense["dense_tok_s_attention_only"] = B / (L * best * 1e-6)
+        res_d, notes = dense_baselines(M, B, hq, hkv, d, Tn, T + total_steps, scale, dense_k, dense_v, q0, dev)
+        dense = {f"{k_}_us_per_layer": round(v_, 3) for k_, v_ in res_d.items()}
+        if notes:
+            dense["notes"] = notes
+        if res_d:
+            best_name = min(res_d, key=res_d.get)
+            dense["best"] = best_name
+            dense["best_dense_us_per_layer"] = round(res_d[best_name], 3)
+            dense["dense_bytes_per_layer"] = U * (Tn * 4 * d + 2 * G * d * 2)
+            dense["best_dense_achieved_gbs"] = round(dense["dense_bytes_per_layer"] / (res_d[best_name] * 1e-6) / 1e9, 1)
+            dense["dense_tok_s_attention_only"] = round(B / (L * res_d[best_name] * 1e-6), 2)
+            dense["layers_rotated"] = len(dense_k)
+        del dense_k, dense_v
 
     # ---- reduce over ranks (max time)
     import torch as _t
-    vals = _t.tensor([ms, attn_us, e2e_ms], dtype=_t.float64, device=dev)
+    vals = _t.tensor([ms, attn_us, e2e_ms, step_ms[0], step_ms[-1]], dtype=_t.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, attn_us, e2e_ms = vals.tolist()
+    ms, attn_us, e2e_ms = vals.tolist()[:3]
 
     bytes_attn = algorithmic_bytes(U, G, n_comp, n_win, kk, kv, append=True)
     peaks = {}
@@ -462,10 +595,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         pass
     tok_s = world * B / (ms * 1e-3)
     per_step_in = L * per_layer * 2
+    nk = caches[0].decode_step_kernel_count()
+    par = f"dp{world} (batch x kv-head units" + (", in-place NCCL all_gather of every layer's output)" if gather
+                                                 else ", no collective)")
     res = {
         "metric": METRIC,
         "value": round(tok_s, 2),
-        "unit": "tokens/s (attention-only decode, 32 layers)" if L == 32 else f"tokens/s (attention-only decode, {L} layers)",
+        "unit": unit_string(L),
         "n_gpus": world, "steps": K_steps, "warmup": W_steps,
         "ms_per_step": round(ms, 4),
         "higher_is_better": True,
@@ -473,21 +609,27 @@ def run_ours(args, cfg, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f16 (fp32 accumulate)",
         "data": "synthetic (seeded splitmix64 -> fp16 ~N(0,1)); no model weights",
-        "config": {"workload": args.workload, "desc": cfg["desc"], "batch_per_gpu": B, "global_batch": B * world,
-                   "num_q_heads": hq, "num_kv_heads": hkv, "head_dim": d, "context": T, "keep_k": kk, "keep_v": kv,
-                   "window": W_WINDOW, "layers": L, "parallelism": f"dp{world} (batch x kv-head units, " + ("in-place all_gather of every layer's output)" if gather else "no collective)"),
-                   "l2": f"inputs larger than L2: {L} layer caches x {caches[0].nbytes / 1e6:.0f} MB"},
+        "config": config_of(args, cfg, world, L, {
+            "parallelism": par,
+            "l2": f"inputs larger than L2: {L} layer caches x {caches[0].nbytes / 1e6:.0f} MB"}),
         "us_per_layer_step": round(ms * 1e3 / L, 3),
+        "step_ms_p10_p50_p90": [round(pct(0.1), 4), round(pct(0.5), 4), round(pct(0.9), 4)],
         "decode_step_us_per_call_events": round(attn_us, 3),  # second pass: events around each call
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": ("mstf_decode_step: mstf_attn_reg_kernel with the fused append + mstf_sk_combine_kernel" if caches[0].decode_step_kernel_count() == 2 else "mstf_decode_step: append_kernel + mstf_attn_kv_kernel + mstf_combine_kernel") + ", CUDA events per call in a second timed pass",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
+                     "frac_of_spec_8tbs": round(achieved / SPEC_HBM_GBS, 4),
+                     "read_peak_gbs": round(read_gbs, 1) if read_gbs else None,
+                     "frac_of_read_peak": round(achieved / read_gbs, 4) if read_gbs else None,
+                     "kernel": ("mstf_decode_step: mstf_attn_warp_kernel (append fused) + mstf_warp_combine_kernel"
+                                if nk == 2 else "mstf_decode_step: append + attention + combine")
+                               + ", CUDA events around each call in a second timed pass",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s",
+                     "read_peak_source": "mstf_dev_read_bandwidth over 4 GiB, 5 passes, measured in this run",
                      "algorithmic_bytes_per_launch": bytes_attn},
-        "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
+        "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": unit_string(L),
                 "h2d_bytes_per_step": per_step_in, "d2h_bytes_per_step": U * G * d * 2,
                 "steps": e2e_steps, "ms_per_step": round(e2e_ms, 4)},
-        "gpu_launches": K_steps * L * caches[0].decode_step_kernel_count(),  # headline pass
+        "gpu_launches": K_steps * L * nk,  # headline pass
         "clocks": clocks,
         "dense_kv": dense,
         "prefill": {"kernel": "prefill_kernel (mstf_prune_compress_kv: a1-a4 bulk over the prompt)",
@@ -496,37 +638,45 @@ def run_ours(args, cfg, rank, world, local_rank):
                     "frac": round(pf_bytes / (pf_us * 1e-6) / 1e9 / peak, 4), "algorithmic_bytes": pf_bytes,
                     "timing": "CUDA events around each layer's call during setup, median over layers 1.."},
     }
+    if gather_us is not None:
+        res["multi_gpu"] = {"kernel_only_us_per_layer": round(attn_us, 3), "gather_us_per_layer": round(gather_us, 3),
+                            "e2e_ms_per_step": round(e2e_ms, 4), "collective": "NCCL all_gather_into_tensor, in place"}
     if dense.get("best_dense_us_per_layer"):
         # our whole step (append + attention, headline pass) vs dense attention alone
         res["speedup_vs_best_dense_attention"] = round(dense["best_dense_us_per_layer"] / (ms * 1e3 / L), 3)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        v, desc, cores = oracle_sample(cfg, seconds=args.cpu_seconds)
-        res["cpu_baseline"] = {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+        v, desc, cores, _, _ = oracle_sample(cfg, seconds=args.cpu_seconds)
+        res["cpu_baseline"] = {"value": round(v, 4), "unit": unit_string(L), "cores": cores, "kind": "oracle",
                                "sample": desc}
     return res
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only). Each step
+    is a bounded sample of the workload: one unit of layer 0 (a decode-step append + fp64
+    Algorithm 1 over its tokens); ms_per_step is that measured sample time, and `value`
+    extrapolates it to the whole job (units x layers), on our arm's metric, unit and config."""
     if rank != 0:
         return None
-    per_step = []
+    per_unit, desc = [], ""
     for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        v, desc, cores = oracle_sample(cfg, seconds=0.0, max_units=1)
-        dt = time.perf_counter() - t0
+        v, desc, cores, t_unit, _ = oracle_sample(cfg, seconds=0.0, max_units=1)
         if s >= args.warmup:
-            per_step.append(v)
-    v = statistics.mean(per_step)
-    B = cfg["batch"]
-    ms = B / v * 1e3
-    return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "desc": cfg["desc"]},
-            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            per_unit.append(t_unit)
+    t_unit = statistics.mean(per_unit)
+    B, U = cfg["batch"], cfg["batch"] * cfg["hkv"]
+    v = B / (t_unit * U * LAYERS)
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": unit_string(LAYERS),
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_unit * 1e3, 3),
+            "ms_per_step_note": "measured time of one step's bounded sample (1 unit of 1 layer); value = "
+                                f"global_batch / (that x {U} units x {LAYERS} layers)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded splitmix64 -> fp16 ~N(0,1)); no model weights",
+            "config": config_of(args, cfg, world, LAYERS, {"parallelism": "CPU oracle, 1 thread"}),
+            "cpu_baseline": {"value": round(v, 6), "unit": unit_string(LAYERS), "cores": cores, "kind": "oracle",
                              "sample": "each step: " + desc},
-            "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(v, 6), "unit": unit_string(LAYERS), "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
 
 
 def main():
@@ -535,11 +685,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=list(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=list(WORKLOADS))
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--no-dense", dest="dense", action="store_false")
-    ap.add_argument("--gather", action="store_true",
-                    help="N>1: all-gather every layer's output into [B][Hq][d] (a10; off by default)")
+    ap.add_argument("--gather", dest="gather", action="store_true", default=None,
+                    help="all-gather every layer's output into [B][Hq][d] (a10; default on for N > 1)")
+    ap.add_argument("--no-gather", dest="gather", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

@@ -188,6 +188,21 @@ int mstf_decode_step(mstf_cache* cache, const void* k_new, const void* v_new, co
  * 3 unfused; negative status for a NULL handle. Host-only. */
 int mstf_decode_step_kernel_count(const mstf_cache* cache);
 
+/* CUDA-graph replay of decode steps (NEXT-1). On a uniform cache (every unit with the same
+ * counters) mstf_decode_step's launches take no argument that depends on the counters: the
+ * kernels read n_comp / n_win from the device, the fused append's flags are cleared by the
+ * step's own combine kernel and the combine advances the device counters. A graph captured
+ * around n_layers x mstf_decode_step therefore replays correctly step after step, but the
+ * replays bypass the handle, so its host mirror no longer follows the device.
+ * mstf_graph_step_check: returns MSTF_OK if `steps` more uniform decode steps fit (every
+ *   unit's compressed capacity), MSTF_ECAPACITY if not, MSTF_EINVAL if the cache is not uniform
+ *   (a captured step would not be the fused, counter-independent one). Host-only.
+ * mstf_graph_step_commit: advances the host mirror by `steps` decode steps that graph replays
+ *   enqueued (same rule as mstf_append_token: the oldest window token is compressed once the
+ *   window is full). Validates like the check first; host-only, no device access.          */
+int mstf_graph_step_check(const mstf_cache* cache, int32_t steps);
+int mstf_graph_step_commit(mstf_cache* cache, int32_t steps);
+
 /* Number of kernels one mstf_sparse_decode_attention call on this cache launches (the
  * attention kernel and the split combine), or a negative status for a NULL handle.
  * Host-only; lets callers count launches. */
@@ -249,6 +264,13 @@ int mstf_query_abs_sum(const void* q, int32_t units, int32_t slots, int32_t grou
  * segments [4], ...} (24 words per CTA) recorded by the last attention launch made with the
  * environment variable MSTF_TRACE set. host: HOST buffer. Synchronous. Errors: ECUDA.        */
 int mstf_dev_trace(void* host, int32_t n);
+
+/* Development only (bench.py's read-only roofline denominator), not part of the hot path:
+ * streams [src, src + bytes) once with 16-byte loads and nothing else (bytes rounded down to a
+ * multiple of 16). src: DEVICE, 16-byte aligned; sink: DEVICE u32 (written only on an
+ * impossible XOR pattern, it keeps the loads alive). Asynchronous on `stream`.
+ * Errors: EINVAL (null / misaligned), ECUDA.                                                 */
+int mstf_dev_read_bandwidth(const void* src, size_t bytes, void* sink, void* stream);
 
 /* Human-readable status (static string). */
 const char* mstf_status_string(int32_t status);

@@ -1,6 +1,7 @@
 // abi.cu -- the extern "C" boundary declared in include/mustafar.h: host-side validation,
 // buffer sizing, the exact host mirror of the per-unit counters, and kernel launches.
 // No device allocation, no synchronisation.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -391,6 +392,30 @@ int mstf_decode_step_kernel_count(const mstf_cache* h) {
   return uniform_counters(h) && plan.sk ? 2 : 3;
 }
 
+// Host mirror after `steps` uniform decode steps (unit 0 stands for every unit): window filling
+// first, then one compression per step.
+static void advance_uniform(int32_t W, int32_t steps, int32_t* nc, int32_t* nw) {
+  if (W == 0) { *nc += steps; return; }
+  const int32_t fill = std::min(steps, W - *nw);
+  *nw += fill;
+  *nc += steps - fill;
+}
+
+int mstf_graph_step_check(const mstf_cache* h, int32_t steps) {
+  if (!h || steps < 0) return MSTF_EINVAL;
+  if (!use_r2(h) || !summarize(h, false).uniform) return MSTF_EINVAL;
+  int32_t nc = h->nc[0], nw = h->nw[0];
+  advance_uniform(h->view.W, steps, &nc, &nw);
+  return nc <= h->view.cap ? MSTF_OK : MSTF_ECAPACITY;
+}
+
+int mstf_graph_step_commit(mstf_cache* h, int32_t steps) {
+  const int st = mstf_graph_step_check(h, steps);
+  if (st != MSTF_OK) return st;
+  for (int32_t u = 0; u < h->view.U; ++u) advance_uniform(h->view.W, steps, &h->nc[u], &h->nw[u]);
+  return MSTF_OK;
+}
+
 static int32_t dense_splits(int32_t units, int32_t t_max) {
   const int32_t blocks = (t_max + 15) / 16;
   int32_t s = (3 * 148 + units - 1) / units;
@@ -480,6 +505,12 @@ int mstf_attention_kernel_count(const mstf_cache* h) {
 // Dev tooling (declared in include/mustafar.h, "Development only"): the per-CTA timeline of the
 // last attention launch made with MSTF_TRACE set.
 int mstf_dev_trace(void* host, int32_t n) { return copy_trace(host, n) == cudaSuccess ? MSTF_OK : MSTF_ECUDA; }
+
+int mstf_dev_read_bandwidth(const void* src, size_t bytes, void* sink, void* stream) {
+  if (!src || !sink || !aligned16(src) || (reinterpret_cast<uintptr_t>(sink) & 3u)) return MSTF_EINVAL;
+  return launch_dev_read(src, bytes, static_cast<uint32_t*>(sink), sm_count(), static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? MSTF_OK : MSTF_ECUDA;
+}
 
 const char* mstf_build_info(void) { return "mustafar-b200 sm_100a (mma.sync m16n8k16, cp.async.bulk, mbarrier)"; }
 

@@ -108,12 +108,13 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
   asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
-// Gather only when the dibit keeps a channel (mask != 0): idle lanes take no bank slot.
+// Gather only when the dibit keeps a channel (mask != 0): idle lanes take no bank slot. The
+// loaded word replaces the address in the same register; a skipped load leaves the address
+// there, which the AND with the (zero) mask clears -- no zeroed register per gather.
 __device__ __forceinline__ uint32_t lds_masked(uint32_t a, uint32_t mask) {
-  uint32_t v = 0;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
-               : "+r"(v) : "r"(a), "r"(mask) : "memory");
-  return v & mask;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p ld.shared.u32 %0, [%0];\n\t}"
+               : "+r"(a) : "r"(mask) : "memory");
+  return a & mask;
 }
 __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -185,23 +186,33 @@ __device__ __forceinline__ void gather8x2(uint32_t hw2, uint32_t base_a_in, uint
 #undef MSTF_G
 }
 
-// Shifted pair arrays of the 16 tokens of one tensor in a stage: token tau's entries
-// Y[m] = (h[m-1], h[m]), m = 0..kp (h[-1] = h[kp] = 0) at ydst + 4 * (tau * SW + m).
-// Task (tau, c) = 8 values: one 16-byte load + the previous word, two 16-byte stores.
+// Shifted pair arrays of the 16 tokens of both tensors in a stage, one token per lane (lanes
+// 0-15: K tokens 0-15, lanes 16-31: V tokens 0-15): Y[m] = (h[m-1], h[m]), m = 0..kp
+// (h[-1] = h[kp] = 0) at ydst + 4 * (tau * sw + m). Odd entries are the raw words, even ones
+// one prmt each; scalar stores (no register shuffling into 16-byte groups). With sw = kp + 2
+// (2 mod 4) and the V region 1 word past a 32-word boundary, the 32 lanes of every store hit 32
+// distinct banks. raw = this lane's token record in the stage.
 template <int NCH>
-__device__ __forceinline__ void build_pairs(uint32_t raw, uint32_t ydst, int nch_rt, int sw, int lane) {
+__device__ __forceinline__ void build_token(uint32_t raw, uint32_t ydst, int nch_rt) {
   const int nch = NCH ? NCH : nch_rt;
+  uint32_t prev = 0;
+  sts32(ydst, 0u);  // Y[0].lo = h[-1] = 0 (hi = h[0], rewritten below)
 #pragma unroll
-  for (int task = lane; task < 16 * nch; task += 32) {
-    const int tau = task / nch, c = task - tau * nch;
-    const uint32_t src = raw + (uint32_t)(tau * nch * 16 + 16 * c);
-    const uint4 a = lds128(src);
-    const uint32_t prev = c > 0 ? lds32(src - 4) : 0u;
-    const uint32_t dst = ydst + 4u * (uint32_t)(tau * sw + 8 * c);
-    sts128(dst, prmt(prev, a.x, 0x5432), a.x, prmt(a.x, a.y, 0x5432), a.y);
-    sts128(dst + 16, prmt(a.y, a.z, 0x5432), a.z, prmt(a.z, a.w, 0x5432), a.w);
-    if (c == nch - 1) sts32(dst + 32, prmt(a.w, 0u, 0x5432));
+  for (int c = 0; c < (NCH ? NCH : 16); ++c) {
+    if (!NCH && c >= nch) break;
+    const uint4 a = lds128(raw + 16 * c);
+    const uint32_t d = ydst + 32u * c;
+    sts32(d, prmt(prev, a.x, 0x5432));
+    sts32(d + 4, a.x);
+    sts32(d + 8, prmt(a.x, a.y, 0x5432));
+    sts32(d + 12, a.y);
+    sts32(d + 16, prmt(a.y, a.z, 0x5432));
+    sts32(d + 20, a.z);
+    sts32(d + 24, prmt(a.z, a.w, 0x5432));
+    sts32(d + 28, a.w);
+    prev = a.w;
   }
+  sts32(ydst + 32u * nch, prmt(prev, 0u, 0x5432));
 }
 
 // ---------------------------------------------------------------- schedule (device side)
@@ -265,9 +276,9 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   const int P = (int)blockIdx.x * p.wpc + warp;
   // per-warp region: [stages kWNst x stage_bytes][pairs K 16 x swk words][pairs V][mbarriers]
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(warp * p.warp_bytes);
-  const uint32_t ypk = wbase + (uint32_t)(kWNst * p.stage_bytes);
-  const uint32_t ypv = ypk + 64u * (uint32_t)p.swk;
-  const uint32_t bar0 = ypv + 64u * (uint32_t)p.swv;
+  const uint32_t ypk = wbase + (uint32_t)(kWNst * p.stage_bytes);  // 128-byte aligned
+  const uint32_t ypv = ypk + ((64u * (uint32_t)p.swk + 127u) & ~127u) + 4u;
+  const uint32_t bar0 = (ypv + 64u * (uint32_t)p.swv + 7u) & ~7u;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kWNst; ++s) mbar_init_u32(bar0 + 8 * s, 1);
@@ -308,8 +319,9 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   // ---- block streams: producer (TMA issue, one block ahead) and consumer walk the same
   // sequence of compressed blocks: segment by segment, unit u's blocks [lo, min(hi, nbc)).
   const int u_first = unit_of_cost(p, x0, cpu);
-  // producer cursor
-  int pu = u_first, pb = 0, pbe = 0, pseq = 0;
+  // producer cursor: unit pu, next block pb, end pbe; pnc = pu's compressed tokens (as the
+  // attention sees them), pwait = the block holding the record the fused append writes (-1: none)
+  int pu = u_first, pb = 0, pbe = 0, pseq = 0, pnc = 0, pwait = -1;
   bool pdone = false;
   auto seg_bounds = [&](int u, int& lo, int& hi, int& nbc, Counters& cn) {
     cn = counters_of(p, u);
@@ -318,30 +330,28 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     lo = item_of_cost(p, max(x0, us) - us, nbc);
     hi = item_of_cost(p, min(x1, ue) - us, nbc);
   };
-  {
+  auto p_unit = [&]() {  // producer enters unit pu
     int lo, hi, nbc;
     Counters cn;
     seg_bounds(pu, lo, hi, nbc, cn);
     pb = lo;
     pbe = min(hi, nbc);
-  }
+    pnc = cn.nc;
+    // fused step with an eviction: record cn.nc - 1 is written by the unit's appender
+    pwait = (p.fuse && (c.W == 0 || cn.nw == c.W) && cn.nc > 0) ? (cn.nc - 1) / 16 : -1;
+  };
+  p_unit();
   // advance the producer to its next compressed block (or done)
   auto p_advance = [&]() {
     while (!pdone && pb >= pbe) {
       ++pu;
       if (pu >= c.U || unit_start(p, pu, cpu) >= x1) { pdone = true; break; }
-      int lo, hi, nbc;
-      Counters cn;
-      seg_bounds(pu, lo, hi, nbc, cn);
-      pb = lo;
-      pbe = min(hi, nbc);
+      p_unit();
     }
   };
-  const size_t kbm_stride = (size_t)kTiles * 8;
   auto p_issue = [&]() {  // lane 0: TMA of block (pu, pb) into stage pseq % kWNst
-    const Counters cn = counters_of(p, pu);
-    const int tok0 = pb * 16, n = min(16, cn.nc - tok0);
-    if (p.fuse && (c.W == 0 || c.n_win[pu] == c.W) && pb == (cn.nc - 1) / 16) {
+    const int tok0 = pb * 16, n = min(16, pnc - tok0);
+    if (pb == pwait) {
       // this block holds the record the step's append writes: wait for it (TMA = async proxy)
       wait_ready(p.ready + pu);
       fence_proxy_async_global();
@@ -351,9 +361,9 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     const size_t rec = (size_t)pu * c.cap + tok0;
     const uint32_t bytes_bm = (uint32_t)n * 16, bytes_k = (uint32_t)n * 2 * p.kpk, bytes_v = (uint32_t)n * 2 * p.kpv;
     mbar_expect_tx_u32(bar, 2 * bytes_bm + bytes_k + bytes_v);
-    bulk_g2s_u32(st, reinterpret_cast<const uint8_t*>(c.bm[0]) + rec * kbm_stride, bytes_bm, bar);
+    bulk_g2s_u32(st, reinterpret_cast<const uint8_t*>(c.bm[0]) + rec * 16, bytes_bm, bar);
     bulk_g2s_u32(st + p.off_kval, c.val[0] + rec * p.kpk, bytes_k, bar);
-    bulk_g2s_u32(st + p.off_vbm, reinterpret_cast<const uint8_t*>(c.bm[1]) + rec * kbm_stride, bytes_bm, bar);
+    bulk_g2s_u32(st + p.off_vbm, reinterpret_cast<const uint8_t*>(c.bm[1]) + rec * 16, bytes_bm, bar);
     bulk_g2s_u32(st + p.off_vval, c.val[1] + rec * p.kpv, bytes_v, bar);
   };
   p_advance();
@@ -364,15 +374,101 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     p_advance();
   }
 
-  // ---- consumer state
-  constexpr int NT = G8 ? 2 : 1;  // n-tiles of heads (4 heads each) in the V product
-  uint32_t qa[8][2 * NT];         // score A operand: [k-step][row g: lo pair, hi pair (, rows g+8)]
+  // ---- consumer state. Score product in the transposed form S^T[token][head] (A = K tokens,
+  // B = q): lane (g, t) ends with tokens g, g+8 of heads 2t, 2t+1 (c0..c3); for G <= 4 the head
+  // columns n are heads n & 3 (duplicated), for G = 8 heads n. movmatrix turns a P^T tile into
+  // lane (g, t) = [head column g][tokens 2t, 2t+1], the B operand of the V product, whose
+  // columns are (head n & 3 (+4 nt), parity n >> 2).
+  constexpr int NT = G8 ? 2 : 1;  // 4-head tiles of the V product
+  uint32_t qf[16];                // B operand of the score MMAs: q[head][32t .. 32t+31]
   float acc[NT][4][4];            // O'[pair][(head, parity)] per V n-tile, 4 m-tiles
-  float m_[NT], l_[NT];
-  const int h0 = g >> 1;          // the score rows of lane (g, t): head g>>1 (and 4 + g>>1 for G = 8)
-  const uint32_t sel_lo = (g & 1) ? 0x1044u : 0x4410u, sel_hi = (g & 1) ? 0x3244u : 0x4432u;
+  float m0, m1, l0, l1;           // softmax state of heads 2t, 2t+1 (log2 domain)
+  const uint32_t par = (uint32_t)(g >> 2);
+  const uint32_t sel_lo = par ? 0x1044u : 0x4410u, sel_hi = par ? 0x3244u : 0x4432u;
+  // build role of this lane: token lane & 15 of K (lanes 0-15) or V (16-31)
+  const uint32_t raw_off = lane < 16 ? (uint32_t)(p.off_kval + (lane & 15) * 2 * p.kpk)
+                                     : (uint32_t)(p.off_vval + (lane & 15) * 2 * p.kpv);
+  const uint32_t ydst = lane < 16 ? ypk + 4u * (uint32_t)((lane & 15) * p.swk) : ypv + 4u * (uint32_t)((lane & 15) * p.swv);
+  const int nch_me = (lane < 16 ? p.kpk : p.kpv) >> 3;
   int qu = -1;
   int cseq = 0;  // compressed blocks consumed
+
+  // a5: S^T (16 tokens x 8 head columns) += K_blk . q^T over the 8 k-steps (two chains)
+  auto scores = [&](float (&sc)[4], const uint32_t (&k0)[16], const uint32_t (&k1)[16]) {
+    float s2[4] = {0.f, 0.f, 0.f, 0.f};
+    sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
+#pragma unroll
+    for (int s = 0; s < 8; s += 2) {
+      mma16816(sc, k0[2 * s], k1[2 * s], k0[2 * s + 1], k1[2 * s + 1], qf[2 * s], qf[2 * s + 1]);
+      mma16816(s2, k0[2 * s + 2], k1[2 * s + 2], k0[2 * s + 3], k1[2 * s + 3], qf[2 * s + 2], qf[2 * s + 3]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sc[i] += s2[i];
+  };
+  // a7: online softmax over the block (tokens g, g+8 valid: vg, vg8), rescale of the
+  // accumulators; bb[nt] = B operand of the V product {k-step 0 lo, hi, k-step 1 lo, hi}
+  auto softmax = [&](const float (&sc)[4], bool vg, bool vg8, uint32_t (&bb)[NT][4]) {
+    const float x0 = vg ? sc[0] * p.scale_log2 : -INFINITY, x1 = vg ? sc[1] * p.scale_log2 : -INFINITY;
+    const float x2 = vg8 ? sc[2] * p.scale_log2 : -INFINITY, x3 = vg8 ? sc[3] * p.scale_log2 : -INFINITY;
+    float b0 = fmaxf(x0, x2), b1 = fmaxf(x1, x3);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      b0 = fmaxf(b0, __shfl_xor_sync(0xffffffffu, b0, o));
+      b1 = fmaxf(b1, __shfl_xor_sync(0xffffffffu, b1, o));
+    }
+    const float n0 = fmaxf(m0, b0), n1 = fmaxf(m1, b1);
+    const float a0 = ex2(m0 - n0), a1 = ex2(m1 - n1);
+    const float p0 = ex2(x0 - n0), p1 = ex2(x1 - n1), p2 = ex2(x2 - n0), p3 = ex2(x3 - n1);
+    l0 = l0 * a0 + (p0 + p2);
+    l1 = l1 * a1 + (p1 + p3);
+    m0 = n0;
+    m1 = n1;
+    // accumulator columns 2t, 2t+1 of tile nt hold heads (2t & 3) + 4 nt, (2t+1 & 3) + 4 nt
+    float aa[NT][2];
+    if constexpr (G8) {
+      const float o0 = __shfl_xor_sync(0xffffffffu, a0, 2), o1 = __shfl_xor_sync(0xffffffffu, a1, 2);
+      aa[0][0] = t < 2 ? a0 : o0; aa[0][1] = t < 2 ? a1 : o1;
+      aa[1][0] = t < 2 ? o0 : a0; aa[1][1] = t < 2 ? o1 : a1;
+    } else {
+      aa[0][0] = a0;
+      aa[0][1] = a1;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      if (!__all_sync(0xffffffffu, aa[nt][0] == 1.f && aa[nt][1] == 1.f)) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[nt][i][0] *= aa[nt][0]; acc[nt][i][1] *= aa[nt][1];
+          acc[nt][i][2] *= aa[nt][0]; acc[nt][i][3] *= aa[nt][1];
+        }
+      }
+    }
+    // P^T tiles (tokens g / g+8, heads 2t, 2t+1) -> P tiles [head g][tokens 2t, 2t+1 (+8)]
+    uint32_t M[2] = {movmatrix_t(pack_half2(p0, p1)), movmatrix_t(pack_half2(p2, p3))};
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      if constexpr (G8) {
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, M[ks], 16);
+        const uint32_t m_lo = g < 4 ? M[ks] : other, m_hi = g < 4 ? other : M[ks];
+        bb[0][2 * ks] = prmt(m_lo, 0u, sel_lo);
+        bb[0][2 * ks + 1] = prmt(m_lo, 0u, sel_hi);
+        bb[1][2 * ks] = prmt(m_hi, 0u, sel_lo);
+        bb[1][2 * ks + 1] = prmt(m_hi, 0u, sel_hi);
+      } else {
+        bb[0][2 * ks] = prmt(M[ks], 0u, sel_lo);
+        bb[0][2 * ks + 1] = prmt(M[ks], 0u, sel_hi);
+      }
+    }
+  };
+  // a8 for k-step ks (tokens 8 ks + 2t (va), 8 ks + 2t + 1 (vb)):
+  // O'[pair][(head, parity)] += V'[pair][(token, e)] . P'
+  auto values_ks = [&](int ks, const uint32_t (&va)[8], const uint32_t (&vb)[8], const uint32_t (&bb)[NT][4]) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+        mma16816(acc[nt][mt], va[mt], va[4 + mt], vb[mt], vb[4 + mt], bb[nt][2 * ks], bb[nt][2 * ks + 1]);
+  };
 
   for (int u = u_first; u < c.U; ++u) {
     const int us = unit_start(p, u, cpu);
@@ -384,94 +480,31 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       if (lane < p.G) *reinterpret_cast<float2*>(p.ws_ml + (((size_t)P + u) * p.G + lane) * 2) = make_float2(-INFINITY, 0.f);
       continue;
     }
-    if (u != qu) {  // q of the unit's heads in the score layout
+    if (u != qu) {  // q of the unit: head column g (g & 3 when G <= 4), channels 32t..32t+31
       qu = u;
+      const int h = G8 ? g : (g & 3);
+      if (h < p.G) {
+        const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + h) * kD + 32 * t);
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int h = h0 + 4 * nt;
-        if (h < p.G) {
-          const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + h) * kD + 32 * t);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint4 x = __ldg(qp + i);
-            qa[2 * i][2 * nt] = x.x; qa[2 * i][2 * nt + 1] = x.y;
-            qa[2 * i + 1][2 * nt] = x.z; qa[2 * i + 1][2 * nt + 1] = x.w;
-          }
-        } else {
-#pragma unroll
-          for (int s = 0; s < 8; ++s) qa[s][2 * nt] = qa[s][2 * nt + 1] = 0u;
+        for (int i = 0; i < 4; ++i) {
+          const uint4 x = __ldg(qp + i);
+          qf[4 * i] = x.x; qf[4 * i + 1] = x.y; qf[4 * i + 2] = x.z; qf[4 * i + 3] = x.w;
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) qf[i] = 0u;
       }
     }
+    m0 = m1 = -INFINITY;
+    l0 = l1 = 0.f;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      m_[nt] = -INFINITY;
-      l_[nt] = 0.f;
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[nt][i][0] = acc[nt][i][1] = acc[nt][i][2] = acc[nt][i][3] = 0.f;
-    }
     if (lane == 0 && hi > nbc && c.W > 0) {  // window rows are read after the unit's records
       l2_prefetch(c.win[0] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
       l2_prefetch(c.win[1] + (size_t)u * c.W * kD, (uint32_t)c.W * kD * 2);
     }
-
-    // a5 + a7 for one block: scores, online softmax, rescale of the accumulators; returns the
-    // B operand of the V product per head tile: bb[ht] = {k-step 0 lo, hi, k-step 1 lo, hi}
-    auto scores = [&](const uint32_t (&kr)[2][16], const bool (&valid)[4], uint32_t (&bb)[NT][4]) {
-      float sc[2][4];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          if constexpr (G8)
-            mma16816(sc[nt], qa[s][0], qa[s][2], qa[s][1], qa[s][3], kr[nt][2 * s], kr[nt][2 * s + 1]);
-          else
-            mma16816(sc[nt], qa[s][0], 0u, qa[s][1], 0u, kr[nt][2 * s], kr[nt][2 * s + 1]);
-        }
-      }
-      // x[i]: token {2t, 2t+1, 8+2t, 9+2t}[i] of head h0 (c0, c1) and head 4 + h0 (c2, c3)
-#pragma unroll
-      for (int ht = 0; ht < NT; ++ht) {
-        float x[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) x[i] = valid[i] ? sc[i >> 1][2 * ht + (i & 1)] * p.scale_log2 : -INFINITY;
-        float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
-        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-        const float mn = fmaxf(m_[ht], bm);
-        const float alpha = ex2(m_[ht] - mn);
-        float pr[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) pr[i] = ex2(x[i] - mn);
-        l_[ht] = l_[ht] * alpha + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
-        m_[ht] = mn;
-        // accumulators of lane (g, t) hold head t (+4 ht): its alpha lives in lane 8t
-        const float a_acc = __shfl_sync(0xffffffffu, alpha, 8 * t);
-        if (!__all_sync(0xffffffffu, a_acc == 1.f)) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc[ht][i][0] *= a_acc; acc[ht][i][1] *= a_acc; acc[ht][i][2] *= a_acc; acc[ht][i][3] *= a_acc;
-          }
-        }
-        // B operand of the V product: column (head g>>1, parity g&1), rows (token, parity)
-        const uint32_t H0 = pack_half2(pr[0], pr[1]), H1 = pack_half2(pr[2], pr[3]);
-        bb[ht][0] = prmt(H0, 0u, sel_lo);
-        bb[ht][1] = prmt(H0, 0u, sel_hi);
-        bb[ht][2] = prmt(H1, 0u, sel_lo);
-        bb[ht][3] = prmt(H1, 0u, sel_hi);
-      }
-    };
-    // a8 for one block: O'[pair][(head, parity)] += V'[pair][(token, e)] . P'
-    auto values = [&](const uint32_t (&vr)[4][8], const uint32_t (&bb)[NT][4]) {
-#pragma unroll
-      for (int ht = 0; ht < NT; ++ht)
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          mma16816(acc[ht][mt], vr[0][mt], vr[0][4 + mt], vr[1][mt], vr[1][4 + mt], bb[ht][0], bb[ht][1]);
-          mma16816(acc[ht][mt], vr[2][mt], vr[2][4 + mt], vr[3][mt], vr[3][4 + mt], bb[ht][2], bb[ht][3]);
-        }
-    };
 
     // -------- compressed blocks [lo, min(hi, nbc))
     const int bend = min(hi, nbc);
@@ -480,8 +513,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes);
       mbar_wait_u32(bar0 + 8 * s, (uint32_t)(cseq / kWNst) & 1u);
       const int nvalid = min(16, cn.nc - b * 16);
-      build_pairs<NK>(st + p.off_kval, ypk, p.kpk >> 3, p.swk, lane);
-      build_pairs<NV>(st + p.off_vval, ypv, p.kpv >> 3, p.swv, lane);
+      build_token<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
       // K bitmap word t of tokens g, g + 8; V half-word g of tokens 2t, 2t+1, 8+2t, 9+2t
       const uint32_t kw0 = g < nvalid ? lds32(st + 16 * g + 4 * t) : 0u;
       const uint32_t kw1 = g + 8 < nvalid ? lds32(st + 16 * (g + 8) + 4 * t) : 0u;
@@ -519,21 +551,22 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
         if (g >= o) iv += y;
       }
       const uint32_t ev = iv - pv;
-      const bool valid[4] = {tk[0] < nvalid, tk[1] < nvalid, tk[2] < nvalid, tk[3] < nvalid};
       uint32_t bb[NT][4];
       {
-        uint32_t kr[2][16];
-        gather16(kw0, ypk + 4u * ((uint32_t)(g * p.swk) + (ek & 0xFFFFu)), kr[0]);
-        gather16(kw1, ypk + 4u * ((uint32_t)((g + 8) * p.swk) + (ek >> 16)), kr[1]);
-        scores(kr, valid, bb);
+        float sc[4];
+        uint32_t k0[16], k1[16];
+        gather16(kw0, ypk + 4u * ((uint32_t)(g * p.swk) + (ek & 0xFFFFu)), k0);
+        gather16(kw1, ypk + 4u * ((uint32_t)((g + 8) * p.swk) + (ek >> 16)), k1);
+        scores(sc, k0, k1);
+        softmax(sc, g < nvalid, g + 8 < nvalid, bb);
       }
-      {
-        uint32_t vr[4][8];
 #pragma unroll
-        for (int x = 0; x < 4; x += 2)
-          gather8x2(hw[x] | (hw[x + 1] << 16), ypv + 4u * ((uint32_t)(tk[x] * p.swv) + ((ev >> (8 * x)) & 0xFFu)),
-                    ypv + 4u * ((uint32_t)(tk[x + 1] * p.swv) + ((ev >> (8 * x + 8)) & 0xFFu)), vr[x], vr[x + 1]);
-        values(vr, bb);
+      for (int ks = 0; ks < 2; ++ks) {
+        uint32_t va[8], vb[8];
+        gather8x2(hw[2 * ks] | (hw[2 * ks + 1] << 16),
+                  ypv + 4u * ((uint32_t)(tk[2 * ks] * p.swv) + ((ev >> (16 * ks)) & 0xFFu)),
+                  ypv + 4u * ((uint32_t)(tk[2 * ks + 1] * p.swv) + ((ev >> (16 * ks + 8)) & 0xFFu)), va, vb);
+        values_ks(ks, va, vb, bb);
       }
     }
 
@@ -557,63 +590,79 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
         };
         if (!__any_sync(0xffffffffu, ok(lane & 15))) continue;
         const int tk[4] = {2 * t, 2 * t + 1, 8 + 2 * t, 9 + 2 * t};
-        bool valid[4];
-#pragma unroll
-        for (int xx = 0; xx < 4; ++xx) valid[xx] = ok(tk[xx]);
         uint32_t bb[NT][4];
         {
-        uint32_t kr[2][16];
+          float sc[4];
+          uint32_t kk[2][16];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const int tok = g + 8 * nt;
-          if (ok(tok)) {
-            const uint4* pp = reinterpret_cast<const uint4*>(wk + (size_t)(row0 + tok) * kD + 32 * t);
+          for (int nt = 0; nt < 2; ++nt) {
+            const int tok = g + 8 * nt;
+            if (ok(tok)) {
+              const uint4* pp = reinterpret_cast<const uint4*>(wk + (size_t)(row0 + tok) * kD + 32 * t);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint4 a = __ldcg(pp + i);
-              kr[nt][4 * i] = a.x; kr[nt][4 * i + 1] = a.y; kr[nt][4 * i + 2] = a.z; kr[nt][4 * i + 3] = a.w;
+              for (int i = 0; i < 4; ++i) {
+                const uint4 a = __ldcg(pp + i);
+                kk[nt][4 * i] = a.x; kk[nt][4 * i + 1] = a.y; kk[nt][4 * i + 2] = a.z; kk[nt][4 * i + 3] = a.w;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) kk[nt][i] = 0u;
             }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) kr[nt][i] = 0u;
           }
+          scores(sc, kk[0], kk[1]);
+          softmax(sc, ok(g), ok(g + 8), bb);
         }
-        scores(kr, valid, bb);
-        }
-        uint32_t vr[4][8];
 #pragma unroll
-        for (int xx = 0; xx < 4; ++xx) {
-          if (valid[xx]) {
-            const uint4* pp = reinterpret_cast<const uint4*>(wv + (size_t)(row0 + tk[xx]) * kD + 16 * g);
-            const uint4 a = __ldcg(pp), b2 = __ldcg(pp + 1);
-            vr[xx][0] = a.x; vr[xx][1] = a.y; vr[xx][2] = a.z; vr[xx][3] = a.w;
-            vr[xx][4] = b2.x; vr[xx][5] = b2.y; vr[xx][6] = b2.z; vr[xx][7] = b2.w;
-          } else {
+        for (int ks = 0; ks < 2; ++ks) {
+          uint32_t vv[2][8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) vr[xx][i] = 0u;
+          for (int e = 0; e < 2; ++e) {
+            const int xx = 2 * ks + e;
+            if (ok(tk[xx])) {
+              const uint4* pp = reinterpret_cast<const uint4*>(wv + (size_t)(row0 + tk[xx]) * kD + 16 * g);
+              const uint4 a = __ldcg(pp), b2 = __ldcg(pp + 1);
+              vv[e][0] = a.x; vv[e][1] = a.y; vv[e][2] = a.z; vv[e][3] = a.w;
+              vv[e][4] = b2.x; vv[e][5] = b2.y; vv[e][6] = b2.z; vv[e][7] = b2.w;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) vv[e][i] = 0u;
+            }
           }
+          values_ks(ks, vv[0], vv[1], bb);
         }
-        values(vr, bb);
       }
     }
 
     // -------- segment partial (slot P + u): m, l (log2 domain), o unnormalised
     const size_t slot = (size_t)P + u;
+    float lt0 = l0, lt1 = l1;
 #pragma unroll
-    for (int ht = 0; ht < NT; ++ht) {
-      float l = l_[ht];
-      l += __shfl_xor_sync(0xffffffffu, l, 1);
-      l += __shfl_xor_sync(0xffffffffu, l, 2);
-      const int hm = h0 + 4 * ht;  // head of this lane's score rows
-      if ((g & 1) == 0 && t == 0 && hm < p.G)
-        *reinterpret_cast<float2*>(p.ws_ml + (slot * p.G + hm) * 2) = make_float2(m_[ht], l);
-      const int ho = t + 4 * ht;   // head of this lane's accumulators
-      if (ho < p.G) {
-        float4* o = reinterpret_cast<float4*>(p.ws_o + (slot * p.G + ho) * kD + 16 * g);
-        o[0] = make_float4(acc[ht][0][0], acc[ht][0][1], acc[ht][1][0], acc[ht][1][1]);
-        o[1] = make_float4(acc[ht][2][0], acc[ht][2][1], acc[ht][3][0], acc[ht][3][1]);
-        o[2] = make_float4(acc[ht][0][2], acc[ht][0][3], acc[ht][1][2], acc[ht][1][3]);
-        o[3] = make_float4(acc[ht][2][2], acc[ht][2][3], acc[ht][3][2], acc[ht][3][3]);
+    for (int o = 4; o < 32; o <<= 1) {
+      lt0 += __shfl_xor_sync(0xffffffffu, lt0, o);
+      lt1 += __shfl_xor_sync(0xffffffffu, lt1, o);
+    }
+    // lanes g = 0: heads 2t, 2t+1 (G <= 4: t < 2 are the real heads; G = 8: every t)
+    if (g == 0) {
+      if (2 * t < p.G && (G8 || t < 2)) *reinterpret_cast<float2*>(p.ws_ml + (slot * p.G + 2 * t) * 2) = make_float2(m0, lt0);
+      if (2 * t + 1 < p.G && (G8 || t < 2)) *reinterpret_cast<float2*>(p.ws_ml + (slot * p.G + 2 * t + 1) * 2) = make_float2(m1, lt1);
+    }
+    // accumulators of tile nt: heads hA = 2(t & 1) + 4 nt (c0, c2), hA + 1 (c1, c3), parity t >> 1;
+    // rows g: channel 16g + 2mt + par, rows g+8: 16g + 8 + 2mt + par
+    const int pp_ = t >> 1;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int hA = 2 * (t & 1) + 4 * nt;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int h = hA + e;
+        if (h < p.G) {
+          float* o = p.ws_o + (slot * p.G + h) * kD + 16 * g + pp_;
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            o[2 * mt] = acc[nt][mt][e];
+            o[8 + 2 * mt] = acc[nt][mt][2 + e];
+          }
+        }
       }
     }
   }
@@ -767,6 +816,28 @@ void* pick_kernel(bool g8) {
 // ---------------------------------------------------------------- host side
 static size_t r256(size_t b) { return (b + 255) / 256 * 256; }
 
+// cudaFuncSetAttribute once per kernel and size (not per call: keeps the host path short and
+// the launch sequence capturable in a CUDA graph after the first, uncaptured, call).
+static cudaError_t set_max_smem(void* kern, int bytes) {
+  static void* keys[32];
+  static int vals[32];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == kern) {
+      if (vals[i] >= bytes) return cudaSuccess;
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) vals[i] = bytes;
+      return e;
+    }
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && n < 32) {
+    keys[n] = kern;
+    vals[n] = bytes;
+    ++n;
+  }
+  return e;
+}
+
 size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count) {
   const size_t slots = (size_t)sm_count * kWMaxWarps + U + 1;
   return r256(kWHdrInts * sizeof(int)) + r256((size_t)U * sizeof(int)) + r256((size_t)(U + 1) * sizeof(int)) +
@@ -775,13 +846,13 @@ size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count) {
 
 bool warp_kernel_supported(int32_t G) { return G >= 1 && G <= 8; }
 
-static int pair_sw(int kp) { return kp + 4; }  // words per token: Y[0..kp], rows 16-byte aligned
+static int pair_sw(int kp) { return kp + 2; }  // words per token: Y[0..kp]; 2 mod 4 (conflict-free build)
 
 int warp_region_bytes(int32_t kpk, int32_t kpv, int* stage_bytes) {
   const int st = 16 * (16 + 2 * kpk) + 16 * (16 + 2 * kpv);
   if (stage_bytes) *stage_bytes = st;
-  const int pairs = 64 * pair_sw(kpk) + 64 * pair_sw(kpv);
-  return (kWNst * st + pairs + 8 * kWNst + 127) / 128 * 128;
+  const int pairs = (64 * pair_sw(kpk) + 127) / 128 * 128 + 4 + 64 * pair_sw(kpv);
+  return (kWNst * st + (pairs + 7) / 8 * 8 + 8 * kWNst + 127) / 128 * 128;
 }
 
 WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t sm_count) {
@@ -867,7 +938,7 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   else if (nk == nv && nk == 2) kern = pick_kernel<2, 2>(g8);
   else kern = pick_kernel<0, 0>(g8);
   void (*kf)(WParams) = reinterpret_cast<void (*)(WParams)>(kern);
-  e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
+  e = set_max_smem(kern, plan.smem);
   if (e != cudaSuccess) return e;
   e = launch_pdl(kf, dim3(plan.grid), dim3(32 * plan.wpc), (size_t)plan.smem, s, p);
   if (e != cudaSuccess) return e;

@@ -316,3 +316,33 @@ cudaError_t launch_append(const CacheView& c, const uint16_t* k_new, const uint1
 }
 
 }  // namespace mstf
+
+// ---------------------------------------------------------------- dev: read-only HBM stream
+// Measurement tool (bench.py's read-only roofline denominator), not part of the hot path:
+// every thread streams 16-byte loads (4 in flight per iteration) and folds them with XOR; the
+// result is stored only if it matches an impossible pattern, so the loads cannot be dropped.
+namespace mstf {
+__global__ void __launch_bounds__(512) mstf_dev_read_kernel(const uint4* __restrict__ src, size_t n16,
+                                                            uint32_t* __restrict__ sink) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t acc = 0;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+                d = __ldcs(src + i + 3 * stride);
+    acc ^= a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ d.x ^ d.y ^ d.z ^ d.w;
+  }
+  for (; i < n16; i += stride) {
+    const uint4 a = __ldcs(src + i);
+    acc ^= a.x ^ a.y ^ a.z ^ a.w;
+  }
+  if (acc == 0x9E3779B9u && threadIdx.x == 0x3FF) sink[0] = acc;
+}
+
+cudaError_t launch_dev_read(const void* src, size_t bytes, uint32_t* sink, int sm_count, cudaStream_t s) {
+  const size_t n16 = bytes / 16;
+  if (n16 == 0) return cudaSuccess;
+  mstf_dev_read_kernel<<<sm_count * 4, 512, 0, s>>>(static_cast<const uint4*>(src), n16, sink);
+  return cudaGetLastError();
+}
+}  // namespace mstf

@@ -130,6 +130,9 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
                                   void* out, int32_t out_f16, float* part_ml, float* part_o, void* ws,
                                   int32_t sm_count, cudaStream_t s);
 
+// dev: read-only HBM stream over [src, src + bytes) (bench.py's read-peak measurement)
+cudaError_t launch_dev_read(const void* src, size_t bytes, uint32_t* sink, int sm_count, cudaStream_t s);
+
 // dev: copy the per-CTA timeline recorded when MSTF_TRACE is set (n = 3 * CTAs words)
 cudaError_t copy_trace(void* host, int n);
 

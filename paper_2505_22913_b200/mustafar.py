@@ -31,6 +31,7 @@ EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "
            "mstf_decode_step_kernel_count", "mstf_attention_kernel_count",
            "mstf_set_key_weights", "mstf_query_abs_sum",
            "mstf_seq_split", "mstf_sparse_decode_attention_partial", "mstf_merge_partials", "mstf_dev_trace",
+           "mstf_dev_read_bandwidth", "mstf_graph_step_check", "mstf_graph_step_commit",
            "mstf_status_string", "mstf_build_info")
 
 
@@ -81,6 +82,9 @@ def lib() -> ctypes.CDLL:
         "mstf_sparse_decode_attention_partial": (ctypes.c_int, [vp, vp, ctypes.c_float, vp, vp, vp, sz, vp]),
         "mstf_merge_partials": (ctypes.c_int, [i32, i32, i32, i32, vp, vp, vp, i32, vp]),
         "mstf_dev_trace": (ctypes.c_int, [vp, i32]),
+        "mstf_dev_read_bandwidth": (ctypes.c_int, [vp, sz, vp, vp]),
+        "mstf_graph_step_check": (ctypes.c_int, [vp, i32]),
+        "mstf_graph_step_commit": (ctypes.c_int, [vp, i32]),
         "mstf_status_string": (ctypes.c_char_p, [i32]),
         "mstf_build_info": (ctypes.c_char_p, []),
     }
@@ -165,6 +169,15 @@ def merge_partials(ml: torch.Tensor, o: torch.Tensor, out=None, out_dtype=torch.
                                                             _dev_ptr(o, torch.float32, "o"),
                                                             _dev_ptr(out, out.dtype, "out"), code, _stream(stream)))
     return out
+
+
+def dev_read_bandwidth(x: torch.Tensor, sink: torch.Tensor, stream=None):
+    """Development only: stream the bytes of x once (read-only HBM roofline measurement)."""
+    if not x.is_cuda or not x.is_contiguous():
+        raise ValueError("x must be a contiguous CUDA tensor")
+    _check("mstf_dev_read_bandwidth", lib().mstf_dev_read_bandwidth(x.data_ptr(), x.numel() * x.element_size(),
+                                                                    _dev_ptr(sink, torch.int32, "sink"),
+                                                                    _stream(stream)))
 
 
 def buffer_bytes(cfg: Config):
@@ -386,3 +399,51 @@ class DenseAttention:
                                                  scale, _dev_ptr(out, out.dtype, "out"), code,
                                                  self._ws.data_ptr(), self._ws.numel(), _stream(stream)))
         return out
+
+
+class DecodeGraph:
+    """A CUDA graph of one decode step over several layer caches (NEXT-1): for every layer,
+    mstf_decode_step(k_new[l], v_new[l], q[l]) -> out[l] -- the fused append + attention launch
+    and the split combine, chained with programmatic dependent launch. Capture records the
+    launches once; replay() re-runs them with no host work per layer. The kernels read the
+    per-unit counters from the device, so step after step the replays see the growing cache;
+    the host mirrors are advanced by mstf_graph_step_commit. Inputs and outputs are the fixed
+    buffers given here: write the next step's q / k_new / v_new into them before replay()."""
+
+    def __init__(self, caches, q, k_new, v_new, out, scale=None, stream=None):
+        self.caches = list(caches)
+        n = len(self.caches)
+        assert len(q) == len(k_new) == len(v_new) == len(out) == n
+        for c in self.caches:
+            _check("mstf_graph_step_check", lib().mstf_graph_step_check(c._h, 1))
+        self.q, self.k_new, self.v_new, self.out = q, k_new, v_new, out
+        self.scale = scale
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.caches[0].device) if stream is None else stream
+        self._stream = s
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.graph.capture_begin()
+            try:
+                for l, c in enumerate(self.caches):
+                    c.decode_step(k_new[l], v_new[l], q[l], scale, out=out[l], stream=s)
+            finally:
+                self.graph.capture_end()
+        # capture enqueued nothing on the device, but decode_step advanced the host mirrors by
+        # one step: step them back by re-syncing from the pre-capture state is not possible, so
+        # the first replay() is the step the capture described (no commit for it)
+        self._pending = 1
+        torch.cuda.current_stream().wait_stream(s)
+
+    def replay(self):
+        """One decode step of every layer (asynchronous on the capture stream's device order:
+        the graph is launched on the current stream)."""
+        if self._pending == 0:
+            for c in self.caches:
+                _check("mstf_graph_step_check", lib().mstf_graph_step_check(c._h, 1))
+        self.graph.replay()
+        if self._pending:
+            self._pending -= 1
+        else:
+            for c in self.caches:
+                _check("mstf_graph_step_commit", lib().mstf_graph_step_commit(c._h, 1))
