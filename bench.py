@@ -372,7 +372,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # warm-up, the headline timed pass (no events between a step's kernels, so programmatic
     # dependent launch overlaps them), a second pass with events around every layer call (the
     # roofline's per-launch time), and the end-to-end pass
-    total_steps = W_steps + 2 * K_steps + 8
+    total_steps = W_steps + 2 * K_steps + 8 + 2
     T0 = T - 1                       # prefill length; the first decode token makes it T
     cap = T0 - W_WINDOW + total_steps + 8
     scale = 1 / math.sqrt(d)
@@ -453,6 +453,29 @@ def run_ours(args, cfg, rank, world, local_rank):
     for s in range(W_steps):
         step(gen[s])
     torch.cuda.synchronize()
+    # CUDA graph of the whole step (NEXT-1): L x mstf_decode_step captured once, replayed every
+    # step on fixed input buffers (the step's inputs are copied in first, one device copy)
+    dgraph, gbuf = None, None
+    if args.graph:
+        gbuf = torch.empty((L, per_layer), dtype=torch.float16, device=dev)
+        view_cache[gbuf.data_ptr()] = [views(gbuf, l) for l in range(L)]
+        gq, gk, gv = (list(x) for x in zip(*view_cache[gbuf.data_ptr()]))
+        dgraph = M.DecodeGraph(caches, gq, gk, gv, outs, scale)
+
+    def run_step(slab, do_gather=gather):
+        """The step as the headline times it: one graph replay (or the eager per-layer calls)."""
+        if dgraph is None:
+            return step(slab, do_gather=do_gather)
+        gbuf.copy_(slab, non_blocking=True)
+        dgraph.replay()
+        if do_gather:
+            for l in range(L):
+                dist.all_gather_into_tensor(full[l], outs[l])
+
+    if dgraph is not None:  # graph warm-up (its first replay is the captured step)
+        for s in range(2):
+            run_step(gen[W_steps - 1])
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     # ---- headline: K steps, device-timed; an event at every step boundary gives p10/p50/p90
@@ -460,7 +483,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     sev = [torch.cuda.Event(enable_timing=True) for _ in range(K_steps + 1)]
     sev[0].record()
     for s in range(K_steps):
-        step(gen[W_steps + s])
+        run_step(gen[W_steps + s])
         sev[s + 1].record()
     torch.cuda.synchronize()
     if world > 1:
@@ -527,7 +550,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 copy_stream.wait_event(consumed[1 - b])  # step s-1 has read that buffer
             h2d(s + 1, 1 - b)
         compute.wait_event(ready[b])
-        step(dev_in[b])
+        run_step(dev_in[b])
         consumed[b].record(compute)
         host_out[s].copy_(outs[L - 1], non_blocking=True)
     f1.record(compute)
@@ -629,7 +652,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 2), "unit": unit_string(L),
                 "h2d_bytes_per_step": per_step_in, "d2h_bytes_per_step": U * G * d * 2,
                 "steps": e2e_steps, "ms_per_step": round(e2e_ms, 4)},
-        "gpu_launches": K_steps * L * nk,  # headline pass
+        "gpu_launches": K_steps * L * nk,  # headline pass (graph replays launch the same kernels)
+        "step_launch": "one CUDA graph replay per step (L x mstf_decode_step captured)" if dgraph is not None
+                       else "eager: L mstf_decode_step calls per step",
         "clocks": clocks,
         "dense_kv": dense,
         "prefill": {"kernel": "prefill_kernel (mstf_prune_compress_kv: a1-a4 bulk over the prompt)",
@@ -691,6 +716,8 @@ def main():
     ap.add_argument("--gather", dest="gather", action="store_true", default=None,
                     help="all-gather every layer's output into [B][Hq][d] (a10; default on for N > 1)")
     ap.add_argument("--no-gather", dest="gather", action="store_false")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the 32 layer calls eagerly instead of replaying one CUDA graph per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

@@ -1,31 +1,30 @@
 // attn_warp.cu -- decode attention directly over the compressed cache (Algorithm 1,
-// P:236-261), one self-contained warp per work item: the r2 kernel.
+// P:236-261), one self-contained warp per work item: the round-2 kernel.
 //
-// Every warp of a persistent grid is an independent stream-K worker:
-//   * its compressed 16-token blocks are streamed from HBM by TMA bulk copies
-//     (cp.async.bulk, four per block: K bitmaps, K values, V bitmaps, V values -- each a
-//     contiguous run of fixed-stride records, R5-R7) into a private 2-stage shared-memory
-//     ring, issued by the warp itself one block ahead, so the only global-load instructions
-//     of the hot loop are those four copies;
-//   * a5 (q.K^T) and a8 (P.V) run on the tensor cores (mma.sync m16n8k16, fp16 x fp16 ->
-//     fp32) with the SAME warp holding both halves, so no K -> V hand-off exists:
-//       scores  S[row][tok] = Q'[row][ch] . K^T[ch][tok]   M = 16 rows = (head, copy) pairs,
-//               N = 8 tokens, K = 16 channels: the B operand of lane (g, t) is token g's
-//               channel pairs of bitmap word t (the lane's own gathers), and the result
-//               C[row g][tok 2t, 2t+1] is exactly what the V step needs in its B operand;
-//       values  O'[pair][(head, parity)] = V'[pair][(tok, e)] . P'[(tok, e)][(head, parity)]
-//               M = 16 channel pairs, K = 8 tokens x 2 parities, N = 4 heads x 2 parities:
-//               P'[(tok, e)][(h, p)] = P[h][tok] if e == p else 0, so every A register is
-//               one token's channel pair (the lane's own gathers, no transposition) and
-//               D[pair][(h, p)] = O[h][2 pair + p];
+// Every warp of a persistent grid (one CTA per SM) is an independent stream-K worker over the
+// concatenated 16-token blocks of all units:
+//   * its compressed blocks are streamed from HBM by TMA bulk copies (cp.async.bulk, four per
+//     block: K bitmaps, K values, V bitmaps, V values -- each a contiguous run of fixed-stride
+//     records, R5-R7) into a private 2-stage shared-memory ring; the warp issues them itself
+//     two blocks ahead, so the hot loop has no global-load instruction;
+//   * expansion ("load as compressed, compute as dense"): one lane per token rewrites
+//     the packed values as a shifted pair array Y[m] = (h[m-1], h[m]); channel pair (2j, 2j+1)
+//     of a bitmap word with exclusive prefix e is then ONE aligned 32-bit load
+//     Y[e + popc(word & bits <= 2j)], masked by the two bitmap bits;
+//   * a5 (q.K^T) and a8 (P.V) on the tensor cores (mma.sync m16n8k16, fp16 x fp16 -> fp32),
+//     both in the same warp (no K -> V hand-off):
+//       scores  S^T[tok][col] = K[tok][ch] . q^T[ch][col]: M = 16 tokens, N = 8 head columns
+//               (heads col & 3 duplicated for G <= 4, heads col for G = 8), K = 16 channels;
+//               the gathered channel pairs are the A operand as they are;
+//       values  O'[pair][(h, p)] = V'[pair][(tok, e)] . P'[(tok, e)][(h, p)], M = 16 channel
+//               pairs, K = 8 tokens x 2 parities, N = 4 heads x 2 parities, with
+//               P'[(tok, e)][(h, p)] = P[h][tok] if e == p else 0: every A register is one
+//               token's gathered channel pair, D[pair][(h, p)] = O[h][2 pair + p]; movmatrix
+//               turns the P^T tile of the scores into this B operand;
 //   * a7 online softmax in the log2 domain (exp2, log2e folded into the scale);
 //   * the dense local window (a6) is read with 128-bit loads in the same loop;
-//   * each (worker, unit) segment writes one partial (m, l, o) slot; the combine kernel
-//     (a9) merges a unit's slots -- see mstf_warp_combine_kernel.
-// Expansion ("load as compressed, compute as dense"): each token's packed values are
-// rewritten in shared memory as a shifted pair array Y[m] = (h[m-1], h[m]) (two 16-byte
-// stores per 8 values); channel pair (2j, 2j+1) of a bitmap word with exclusive prefix e is
-// then ONE aligned 32-bit load Y[e + popc(word & bits <= 2j)], masked by the two bitmap bits.
+//   * each (worker, unit) segment writes one partial (m, l, o) slot; the combine kernel (a9)
+//     merges a unit's slots.
 //
 // Fused decode step (mstf_decode_step, uniform caches): the worker that owns a unit's first
 // cost unit also appends that unit's new token (a4) before its attention work and publishes
@@ -111,9 +110,17 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
 // Gather only when the dibit keeps a channel (mask != 0): idle lanes take no bank slot. The
 // loaded word replaces the address in the same register; a skipped load leaves the address
 // there, which the AND with the (zero) mask clears -- no zeroed register per gather.
+// MSTF_GATHER_PRED=0 (dev A/B): every lane loads (one instruction less, more bank conflicts).
+#ifndef MSTF_GATHER_PRED
+#define MSTF_GATHER_PRED 1
+#endif
 __device__ __forceinline__ uint32_t lds_masked(uint32_t a, uint32_t mask) {
+#if MSTF_GATHER_PRED
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p ld.shared.u32 %0, [%0];\n\t}"
                : "+r"(a) : "r"(mask) : "memory");
+#else
+  asm volatile("ld.shared.u32 %0, [%0];" : "+r"(a) : : "memory");
+#endif
   return a & mask;
 }
 __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -320,8 +327,11 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   // sequence of compressed blocks: segment by segment, unit u's blocks [lo, min(hi, nbc)).
   const int u_first = unit_of_cost(p, x0, cpu);
   // producer cursor: unit pu, next block pb, end pbe; pnc = pu's compressed tokens (as the
-  // attention sees them), pwait = the block holding the record the fused append writes (-1: none)
+  // attention sees them), pwait = the block holding the record the fused append writes (-1: none);
+  // g_* = global addresses of block pb's four runs (K bitmaps, K values, V bitmaps, V values),
+  // advanced by one block per issue
   int pu = u_first, pb = 0, pbe = 0, pseq = 0, pnc = 0, pwait = -1;
+  const uint8_t *g_kbm = nullptr, *g_kv = nullptr, *g_vbm = nullptr, *g_vv = nullptr;
   bool pdone = false;
   auto seg_bounds = [&](int u, int& lo, int& hi, int& nbc, Counters& cn) {
     cn = counters_of(p, u);
@@ -339,10 +349,20 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     pnc = cn.nc;
     // fused step with an eviction: record cn.nc - 1 is written by the unit's appender
     pwait = (p.fuse && (c.W == 0 || cn.nw == c.W) && cn.nc > 0) ? (cn.nc - 1) / 16 : -1;
+    const size_t rec = (size_t)pu * c.cap + (size_t)pb * 16;
+    g_kbm = reinterpret_cast<const uint8_t*>(c.bm[0]) + rec * 16;
+    g_vbm = reinterpret_cast<const uint8_t*>(c.bm[1]) + rec * 16;
+    g_kv = reinterpret_cast<const uint8_t*>(c.val[0]) + rec * 2 * p.kpk;
+    g_vv = reinterpret_cast<const uint8_t*>(c.val[1]) + rec * 2 * p.kpv;
   };
   p_unit();
   // advance the producer to its next compressed block (or done)
   auto p_advance = [&]() {
+    ++pb;
+    g_kbm += 256;
+    g_vbm += 256;
+    g_kv += 32 * p.kpk;
+    g_vv += 32 * p.kpv;
     while (!pdone && pb >= pbe) {
       ++pu;
       if (pu >= c.U || unit_start(p, pu, cpu) >= x1) { pdone = true; break; }
@@ -350,27 +370,29 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     }
   };
   auto p_issue = [&]() {  // lane 0: TMA of block (pu, pb) into stage pseq % kWNst
-    const int tok0 = pb * 16, n = min(16, pnc - tok0);
+    const uint32_t n = (uint32_t)min(16, pnc - pb * 16);
     if (pb == pwait) {
       // this block holds the record the step's append writes: wait for it (TMA = async proxy)
       wait_ready(p.ready + pu);
       fence_proxy_async_global();
     }
-    const int s = pseq % kWNst;
+    const int s = pseq & (kWNst - 1);
     const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes), bar = bar0 + 8 * s;
-    const size_t rec = (size_t)pu * c.cap + tok0;
-    const uint32_t bytes_bm = (uint32_t)n * 16, bytes_k = (uint32_t)n * 2 * p.kpk, bytes_v = (uint32_t)n * 2 * p.kpv;
+    const uint32_t bytes_bm = n * 16, bytes_k = n * 2 * p.kpk, bytes_v = n * 2 * p.kpv;
     mbar_expect_tx_u32(bar, 2 * bytes_bm + bytes_k + bytes_v);
-    bulk_g2s_u32(st, reinterpret_cast<const uint8_t*>(c.bm[0]) + rec * 16, bytes_bm, bar);
-    bulk_g2s_u32(st + p.off_kval, c.val[0] + rec * p.kpk, bytes_k, bar);
-    bulk_g2s_u32(st + p.off_vbm, reinterpret_cast<const uint8_t*>(c.bm[1]) + rec * 16, bytes_bm, bar);
-    bulk_g2s_u32(st + p.off_vval, c.val[1] + rec * p.kpv, bytes_v, bar);
+    bulk_g2s_u32(st, g_kbm, bytes_bm, bar);
+    bulk_g2s_u32(st + p.off_kval, g_kv, bytes_k, bar);
+    bulk_g2s_u32(st + p.off_vbm, g_vbm, bytes_bm, bar);
+    bulk_g2s_u32(st + p.off_vval, g_vv, bytes_v, bar);
   };
-  p_advance();
+  while (!pdone && pb >= pbe) {  // first unit may hold no compressed block of this range
+    ++pu;
+    if (pu >= c.U || unit_start(p, pu, cpu) >= x1) { pdone = true; break; }
+    p_unit();
+  }
   for (int k = 0; k < kWNst && !pdone; ++k) {
     if (lane == 0) p_issue();
     ++pseq;
-    ++pb;
     p_advance();
   }
 
@@ -509,7 +531,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     // -------- compressed blocks [lo, min(hi, nbc))
     const int bend = min(hi, nbc);
     for (int b = lo; b < bend; ++b, ++cseq) {
-      const int s = cseq % kWNst;
+      const int s = cseq & (kWNst - 1);
       const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes);
       mbar_wait_u32(bar0 + 8 * s, (uint32_t)(cseq / kWNst) & 1u);
       const int nvalid = min(16, cn.nc - b * 16);
@@ -530,7 +552,6 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
           p_issue();
         }
         ++pseq;
-        ++pb;
         p_advance();
       }
       // exclusive prefixes: K over the 4 words of a token (lanes t), V over the 8 half-words

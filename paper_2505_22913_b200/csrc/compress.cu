@@ -51,7 +51,7 @@ __device__ __forceinline__ uint32_t __half2_as_u32(__half2 x) { return *reinterp
 __device__ __forceinline__ uint32_t shfl_down8(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d, 8); }
 __device__ __forceinline__ uint32_t shfl_up8(uint32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d, 8); }
 
-__global__ void __launch_bounds__(256) prefill_kernel(CacheView c, const uint16_t* __restrict__ k,
+__global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint16_t* __restrict__ k,
                                                       const uint16_t* __restrict__ v, int T) {
   const int lane = threadIdx.x & 31, q = lane >> 3, r = lane & 7;
   // byte_perm selectors: put byte 3 (resp. 2) of a word into byte q, zeros elsewhere; take byte q
@@ -323,7 +323,7 @@ cudaError_t launch_append(const CacheView& c, const uint16_t* k_new, const uint1
 // result is stored only if it matches an impossible pattern, so the loads cannot be dropped.
 namespace mstf {
 __global__ void __launch_bounds__(512) mstf_dev_read_kernel(const uint4* __restrict__ src, size_t n16,
-                                                            uint32_t* __restrict__ sink) {
+                                                            uint32_t* __restrict__ sink, uint32_t magic) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t acc = 0;
@@ -336,13 +336,13 @@ __global__ void __launch_bounds__(512) mstf_dev_read_kernel(const uint4* __restr
     const uint4 a = __ldcs(src + i);
     acc ^= a.x ^ a.y ^ a.z ^ a.w;
   }
-  if (acc == 0x9E3779B9u && threadIdx.x == 0x3FF) sink[0] = acc;
+  if (acc == magic) sink[0] = acc;  // magic is a run-time value: the loads cannot be dropped
 }
 
 cudaError_t launch_dev_read(const void* src, size_t bytes, uint32_t* sink, int sm_count, cudaStream_t s) {
   const size_t n16 = bytes / 16;
   if (n16 == 0) return cudaSuccess;
-  mstf_dev_read_kernel<<<sm_count * 4, 512, 0, s>>>(static_cast<const uint4*>(src), n16, sink);
+  mstf_dev_read_kernel<<<sm_count * 4, 512, 0, s>>>(static_cast<const uint4*>(src), n16, sink, 0x9E3779B9u);
   return cudaGetLastError();
 }
 }  // namespace mstf

@@ -85,3 +85,42 @@ def test_shard_ranges_cover_units_exactly():
             assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
             sizes = [b - a for a, b in got]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _gather_worker(rank, world, port, U, G, L, out_path):
+    """Exactly bench.py's a10 data path: every layer's output tensor is a slice
+    full[l][rank*U_r:(rank+1)*U_r] of the [B_global][Hq][d] buffer, written in place by the
+    rank's step, then dist.all_gather_into_tensor(full[l], slice) fills the other ranks' rows."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d = 128
+    Ur = U // world
+    full = [torch.empty(world * Ur, G, d, dtype=torch.float16) for _ in range(L)]
+    outs = [f[rank * Ur:(rank + 1) * Ur] for f in full]
+    for l in range(L):
+        # the rank's "step" writes its output slice in place (what decode_step(out=outs[l]) does)
+        outs[l].copy_(torch.arange(Ur * G * d, dtype=torch.float32).view(Ur, G, d) * 0.001 + rank + 10 * l)
+        assert outs[l].data_ptr() == full[l].data_ptr() + rank * Ur * G * d * 2  # a view, not a copy
+        dist.all_gather_into_tensor(full[l], outs[l])
+    if rank == 0:
+        np.save(out_path, torch.stack(full).float().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_inplace_output_gather_slicing(tmp_path, world):
+    """The in-place NCCL all-gather bench.py runs by default for N > 1, with
+    gloo on CPU: after the gather every rank's [B][Hq][d] buffer holds each rank's slice in
+    rank order (contiguous unit ranges, mstf_shard_units), for every layer."""
+    U, G, L = 8, 4, 3
+    out_path = str(tmp_path / "full.npy")
+    mp.spawn(_gather_worker, args=(world, _free_port(), U, G, L, out_path), nprocs=world, join=True)
+    got = np.load(out_path)
+    Ur, d = U // world, 128
+    base = (np.arange(Ur * G * d, dtype=np.float32).reshape(Ur, G, d) * 0.001)
+    for l in range(L):
+        for r in range(world):
+            exp = (torch.from_numpy(base) + r + 10 * l).half().float().numpy()
+            assert np.array_equal(got[l, r * Ur:(r + 1) * Ur], exp), (l, r)
