@@ -457,12 +457,11 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      if (!__all_sync(0xffffffffu, aa[nt][0] == 1.f && aa[nt][1] == 1.f)) {
+      // unconditional (FMA pipe, branch-free: loads of the next phase can be scheduled across)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[nt][i][0] *= aa[nt][0]; acc[nt][i][1] *= aa[nt][1];
-          acc[nt][i][2] *= aa[nt][0]; acc[nt][i][3] *= aa[nt][1];
-        }
+      for (int i = 0; i < 4; ++i) {
+        acc[nt][i][0] *= aa[nt][0]; acc[nt][i][1] *= aa[nt][1];
+        acc[nt][i][2] *= aa[nt][0]; acc[nt][i][3] *= aa[nt][1];
       }
     }
     // P^T tiles (tokens g / g+8, heads 2t, 2t+1) -> P tiles [head g][tokens 2t, 2t+1 (+8)]
@@ -573,21 +572,25 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       }
       const uint32_t ev = iv - pv;
       uint32_t bb[NT][4];
+      // V k-step 0 gathers are issued before the softmax (they do not depend on it), so their
+      // shared-memory latency overlaps the shuffles and exp2 of the softmax
+      uint32_t va0[8], vb0[8];
       {
         float sc[4];
         uint32_t k0[16], k1[16];
         gather16(kw0, ypk + 4u * ((uint32_t)(g * p.swk) + (ek & 0xFFFFu)), k0);
         gather16(kw1, ypk + 4u * ((uint32_t)((g + 8) * p.swk) + (ek >> 16)), k1);
         scores(sc, k0, k1);
+        gather8x2(hw[0] | (hw[1] << 16), ypv + 4u * ((uint32_t)(tk[0] * p.swv) + (ev & 0xFFu)),
+                  ypv + 4u * ((uint32_t)(tk[1] * p.swv) + ((ev >> 8) & 0xFFu)), va0, vb0);
         softmax(sc, g < nvalid, g + 8 < nvalid, bb);
       }
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
+      values_ks(0, va0, vb0, bb);
+      {
         uint32_t va[8], vb[8];
-        gather8x2(hw[2 * ks] | (hw[2 * ks + 1] << 16),
-                  ypv + 4u * ((uint32_t)(tk[2 * ks] * p.swv) + ((ev >> (16 * ks)) & 0xFFu)),
-                  ypv + 4u * ((uint32_t)(tk[2 * ks + 1] * p.swv) + ((ev >> (16 * ks + 8)) & 0xFFu)), va, vb);
-        values_ks(ks, va, vb, bb);
+        gather8x2(hw[2] | (hw[3] << 16), ypv + 4u * ((uint32_t)(tk[2] * p.swv) + ((ev >> 16) & 0xFFu)),
+                  ypv + 4u * ((uint32_t)(tk[3] * p.swv) + (ev >> 24)), va, vb);
+        values_ks(1, va, vb, bb);
       }
     }
 
@@ -884,7 +887,8 @@ WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t k
   if (wmax > wcap) wmax = wcap;
   if (wmax < 1) wmax = 1;
   // >= ~4 cost units per worker (each worker pays a segment prologue and writes a partial)
-  const int64_t qmin = 4;
+  int64_t qmin = 4;
+  if (const char* e = std::getenv("MSTF_QMIN")) qmin = std::max(1, std::atoi(e));  // dev A/B
   int64_t workers = (total_cost + qmin - 1) / qmin;
   if (workers < 1) workers = 1;
   int grid = sm_count, wpc = wmax;
