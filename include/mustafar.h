@@ -259,12 +259,6 @@ int mstf_set_key_weights(mstf_cache* cache, const float* w);
 int mstf_query_abs_sum(const void* q, int32_t units, int32_t slots, int32_t group, int32_t head_dim,
                        float* w, void* stream);
 
-/* Development only (tools/trace_ctas.py), not part of the hot path: copies up to n u64 words
- * of the per-CTA/per-worker timeline {start ns, -, smid, -, K-warp end ns [4], V-warp end ns [4],
- * segments [4], ...} (24 words per CTA) recorded by the last attention launch made with the
- * environment variable MSTF_TRACE set. host: HOST buffer. Synchronous. Errors: ECUDA.        */
-int mstf_dev_trace(void* host, int32_t n);
-
 /* Development only (bench.py's read-only roofline denominator), not part of the hot path:
  * streams [src, src + bytes) once with 16-byte loads and nothing else (bytes rounded down to a
  * multiple of 16). src: DEVICE, 16-byte aligned; sink: DEVICE u32 (written only on an

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libmustafar.so")
-SOURCES = ["abi.cu", "compress.cu", "attention.cu", "attn_warp.cu"]
+SOURCES = ["abi.cu", "compress.cu", "attn_warp.cu", "dense.cu"]
 HEADERS = ["kernels.cuh", "ptx.cuh", "compress_dev.cuh"]
 
 NVCC_FLAGS = [

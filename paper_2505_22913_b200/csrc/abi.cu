@@ -17,7 +17,6 @@ struct mstf_cache {
   mstf_config cfg;
   CacheView view;
   std::vector<int32_t> nc, nw;  // exact host mirror of n_comp / n_win
-  int32_t max_splits;
 };
 
 namespace {
@@ -105,7 +104,6 @@ int mstf_cache_create(const mstf_config* c, void* const buffers[MSTF_NUM_BUFFERS
   v.kpad[1] = mstf_k_pad(c->keep_v);
   h->nc.assign(v.U, 0);
   h->nw.assign(v.U, 0);
-  h->max_splits = max_splits_for(v.U, c->capacity);
   *out = h;
   return MSTF_OK;
 }
@@ -165,23 +163,10 @@ int mstf_append_token(mstf_cache* h, const void* k_new, const void* v_new, void*
 
 size_t mstf_workspace_bytes(const mstf_cache* h) {
   if (!h) return 0;
-  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
-  const size_t a = attention_ws_bytes(h->view.U, G, h->max_splits);
-  const size_t b = warp_ws_bytes(h->view.U, G, sm_count());
-  return a > b ? a : b;
+  return warp_ws_bytes(h->view.U, h->cfg.num_q_heads / h->cfg.num_kv_heads, sm_count());
 }
 
 namespace {
-// r2 attention kernel (attn_warp.cu) unless MSTF_ATTN=r1 (dev A/B against the round-1 kernels);
-// read once per process.
-bool use_r2(const mstf_cache* h) {
-  static const bool r1 = [] {
-    const char* e = std::getenv("MSTF_ATTN");
-    return e && std::strcmp(e, "r1") == 0;
-  }();
-  return !r1 && warp_kernel_supported(h->cfg.num_q_heads / h->cfg.num_kv_heads);
-}
-
 // Host-mirror summary of the counters as the attention will see them (after == true: after one
 // decode-step append): stream-K total cost, whether every unit is equal, whether one is empty.
 struct MirrorSummary {
@@ -203,7 +188,7 @@ MirrorSummary summarize(const mstf_cache* h, bool after) {
   return r;
 }
 
-int launch_r2(const mstf_cache* h, const MirrorSummary& ms, bool fuse, const void* k_new, const void* v_new,
+int launch_attention(const mstf_cache* h, const MirrorSummary& ms, bool fuse, const void* k_new, const void* v_new,
               const void* q, float scale, void* out, int32_t out_dtype, float* part_ml, float* part_o, void* ws,
               void* stream) {
   const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
@@ -215,31 +200,6 @@ int launch_r2(const mstf_cache* h, const MirrorSummary& ms, bool fuse, const voi
   return e == cudaSuccess ? MSTF_OK : MSTF_ECUDA;
 }
 
-// Attention plan from the host mirror (counters as they will be when the kernels run).
-int make_plan(const mstf_cache* h, const std::vector<int32_t>& nc, const std::vector<int32_t>& nw, AttnPlan* plan) {
-  int32_t max_comp = 0;
-  int64_t total_items = 0;
-  int32_t uniform_items = sk_unit_cost(nc[0], h->view.W);
-  for (int32_t u = 0; u < h->view.U; ++u) {
-    if (nc[u] + nw[u] == 0) return MSTF_EEMPTY;
-    if (nc[u] > max_comp) max_comp = nc[u];
-    const int32_t items = sk_unit_cost(nc[u], h->view.W);
-    total_items += items;
-    if (items != uniform_items) uniform_items = 0;
-  }
-  *plan = plan_attention(h->view.U, max_comp, total_items, uniform_items, h->view.kpad[0], h->view.kpad[1],
-                         sm_count());
-  if (const char* env = std::getenv("MSTF_SCHED")) {  // tuning override: "split" forces the split grid
-    if (std::strcmp(env, "split") == 0) plan->sk = 0;
-  }
-  if (const char* env = std::getenv("MSTF_SPLITS")) {  // tuning override (not part of the ABI contract)
-    const int v = std::atoi(env);
-    if (v > 0) plan->splits = v;
-  }
-  if (plan->splits > h->max_splits) plan->splits = h->max_splits;
-  return MSTF_OK;
-}
-
 int check_attention_args(const mstf_cache* h, const void* q, const void* out, int32_t out_dtype, const void* ws,
                          size_t ws_bytes) {
   if (!h || !q || !out || !aligned16(q)) return MSTF_EINVAL;
@@ -249,42 +209,15 @@ int check_attention_args(const mstf_cache* h, const void* q, const void* out, in
   return MSTF_OK;
 }
 
-// Every unit has the same counters (the fused decode step's precondition).
-bool uniform_counters(const mstf_cache* h) {
-  for (int32_t u = 1; u < h->view.U; ++u)
-    if (h->nc[u] != h->nc[0] || h->nw[u] != h->nw[0]) return false;
-  return true;
-}
-
-// Stamp of a fused step's ready flags: unique across calls and caches of the process.
-int32_t next_epoch() {
-  static std::atomic<int32_t> e{0};
-  int32_t v = ++e;
-  if (v <= 0) {  // wrapped after 2^31 calls
-    e = 1;
-    v = 1;
-  }
-  return v;
-}
 }  // namespace
 
 int mstf_sparse_decode_attention(const mstf_cache* h, const void* q, float scale, void* out, int32_t out_dtype,
                                  void* ws, size_t ws_bytes, void* stream) {
   const int st = check_attention_args(h, q, out, out_dtype, ws, ws_bytes);
   if (st != MSTF_OK) return st;
-  if (use_r2(h)) {
-    const MirrorSummary ms = summarize(h, false);
-    if (ms.empty) return MSTF_EEMPTY;
-    return launch_r2(h, ms, false, nullptr, nullptr, q, scale, out, out_dtype, nullptr, nullptr, ws, stream);
-  }
-  AttnPlan plan;
-  const int sp = make_plan(h, h->nc, h->nw, &plan);
-  if (sp != MSTF_OK) return sp;
-  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
-  if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, out,
-                              out_dtype == MSTF_OUT_F16, ws, static_cast<cudaStream_t>(stream)) != cudaSuccess)
-    return MSTF_ECUDA;
-  return MSTF_OK;
+  const MirrorSummary ms = summarize(h, false);
+  if (ms.empty) return MSTF_EEMPTY;
+  return launch_attention(h, ms, false, nullptr, nullptr, q, scale, out, out_dtype, nullptr, nullptr, ws, stream);
 }
 
 int mstf_sparse_decode_attention_partial(const mstf_cache* h, const void* q, float scale, float* ml, float* o,
@@ -298,18 +231,9 @@ int mstf_sparse_decode_attention_partial(const mstf_cache* h, const void* q, flo
   if (all_empty)  // a shard that holds no token of the sequence (e.g. T < world): the merge identity
     return launch_empty_partials(ml, o, h->view.U * G, static_cast<cudaStream_t>(stream)) == cudaSuccess
                ? MSTF_OK : MSTF_ECUDA;
-  if (use_r2(h)) {
-    const MirrorSummary ms = summarize(h, false);
-    if (ms.empty) return MSTF_EEMPTY;
-    return launch_r2(h, ms, false, nullptr, nullptr, q, scale, nullptr, MSTF_OUT_F32, ml, o, ws, stream);
-  }
-  AttnPlan plan;
-  const int sp = make_plan(h, h->nc, h->nw, &plan);
-  if (sp != MSTF_OK) return sp;
-  if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, nullptr, 0, ws,
-                              static_cast<cudaStream_t>(stream), nullptr, ml, o) != cudaSuccess)
-    return MSTF_ECUDA;
-  return MSTF_OK;
+  const MirrorSummary ms = summarize(h, false);
+  if (ms.empty) return MSTF_EEMPTY;
+  return launch_attention(h, ms, false, nullptr, nullptr, q, scale, nullptr, MSTF_OUT_F32, ml, o, ws, stream);
 }
 
 int mstf_merge_partials(int32_t n, int32_t units, int32_t group, int32_t head_dim, const float* ml, const float* o,
@@ -330,66 +254,25 @@ int mstf_decode_step(mstf_cache* h, const void* k_new, const void* v_new, const 
   const int32_t U = h->view.U, W = h->view.W;
   for (int32_t u = 0; u < U; ++u)
     if ((W == 0 || h->nw[u] == W) && h->nc[u] + 1 > h->view.cap) return MSTF_ECAPACITY;
-  if (use_r2(h)) {
-    const MirrorSummary ms = summarize(h, true);  // counters after the append (a4)
-    if (ms.empty) return MSTF_EEMPTY;
-    if (!ms.uniform) {  // ragged cache: the two calls in sequence
-      const int sa = mstf_append_token(h, k_new, v_new, stream);
-      if (sa != MSTF_OK) return sa;
-      return mstf_sparse_decode_attention(h, q, scale, out, out_dtype, ws, ws_bytes, stream);
-    }
-    const int r = launch_r2(h, ms, true, k_new, v_new, q, scale, out, out_dtype, nullptr, nullptr, ws, stream);
-    if (r != MSTF_OK) return r;
-    for (int32_t u = 0; u < U; ++u) {  // the combine kernel advances the device counters the same way
-      if (W == 0 || h->nw[u] == W) h->nc[u] += 1; else h->nw[u] += 1;
-    }
-    return MSTF_OK;
-  }
-  // counters after the append (a4)
-  const bool uniform = uniform_counters(h);
-  std::vector<int32_t> nc = h->nc, nw = h->nw;
-  for (int32_t u = 0; u < U; ++u) {
-    if (W == 0 || nw[u] == W) nc[u] += 1; else nw[u] += 1;
-  }
-  AttnPlan plan;
-  const int sp = make_plan(h, nc, nw, &plan);
-  if (sp != MSTF_OK) return sp;
-  if (!uniform || !plan.sk) {  // ragged cache or TMA kernel: the two launches in sequence
+  const MirrorSummary ms = summarize(h, true);  // counters after the append (a4)
+  if (ms.empty) return MSTF_EEMPTY;
+  if (!ms.uniform) {  // ragged cache: the two calls in sequence
     const int sa = mstf_append_token(h, k_new, v_new, stream);
     if (sa != MSTF_OK) return sa;
     return mstf_sparse_decode_attention(h, q, scale, out, out_dtype, ws, ws_bytes, stream);
   }
-  FuseArgs fa;
-  fa.k_new = static_cast<const uint16_t*>(k_new);
-  fa.v_new = static_cast<const uint16_t*>(v_new);
-  fa.nc_old = h->nc[0];
-  fa.nw_old = h->nw[0];
-  fa.unc = nc[0];
-  fa.unw = nw[0];
-  fa.evict = (W == 0 || h->nw[0] == W) ? 1 : 0;
-  fa.epoch = next_epoch();
-  const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
-  if (launch_sparse_attention(h->view, plan, G, static_cast<const uint16_t*>(q), scale, out,
-                              out_dtype == MSTF_OUT_F16, ws, static_cast<cudaStream_t>(stream), &fa) != cudaSuccess)
-    return MSTF_ECUDA;
-  h->nc = nc;
-  h->nw = nw;
+  const int r = launch_attention(h, ms, true, k_new, v_new, q, scale, out, out_dtype, nullptr, nullptr, ws, stream);
+  if (r != MSTF_OK) return r;
+  for (int32_t u = 0; u < U; ++u) {  // the combine kernel advances the device counters the same way
+    if (W == 0 || h->nw[u] == W) h->nc[u] += 1; else h->nw[u] += 1;
+  }
   return MSTF_OK;
 }
 
 int mstf_decode_step_kernel_count(const mstf_cache* h) {
   if (!h) return MSTF_EINVAL;
-  if (use_r2(h))  // fused: attention (append inside) + combine; ragged: append + prefix + attention + combine
-    return summarize(h, true).uniform ? 2 : 4;
-  // mirrors mstf_decode_step: fused (register kernel + combine) or append + attention + combine
-  const int32_t U = h->view.U, W = h->view.W;
-  std::vector<int32_t> nc = h->nc, nw = h->nw;
-  for (int32_t u = 0; u < U; ++u) {
-    if (W == 0 || nw[u] == W) nc[u] += 1; else nw[u] += 1;
-  }
-  AttnPlan plan;
-  if (make_plan(h, nc, nw, &plan) != MSTF_OK) return 3;
-  return uniform_counters(h) && plan.sk ? 2 : 3;
+  // fused: attention (append inside) + combine; ragged: append + cost prefix + attention + combine
+  return summarize(h, true).uniform ? 2 : 4;
 }
 
 // Host mirror after `steps` uniform decode steps (unit 0 stands for every unit): window filling
@@ -403,7 +286,7 @@ static void advance_uniform(int32_t W, int32_t steps, int32_t* nc, int32_t* nw) 
 
 int mstf_graph_step_check(const mstf_cache* h, int32_t steps) {
   if (!h || steps < 0) return MSTF_EINVAL;
-  if (!use_r2(h) || !summarize(h, false).uniform) return MSTF_EINVAL;
+  if (!summarize(h, false).uniform) return MSTF_EINVAL;
   int32_t nc = h->nc[0], nw = h->nw[0];
   advance_uniform(h->view.W, steps, &nc, &nw);
   return nc <= h->view.cap ? MSTF_OK : MSTF_ECAPACITY;
@@ -426,7 +309,7 @@ static int32_t dense_splits(int32_t units, int32_t t_max) {
 
 size_t mstf_dense_workspace_bytes(int32_t units, int32_t group, int32_t head_dim, int32_t t_max) {
   if (units < 1 || group < 1 || head_dim != kD || t_max < 1) return 0;
-  return attention_ws_bytes(units, group, dense_splits(units, t_max));
+  return dense_ws_bytes(units, group, dense_splits(units, t_max));
 }
 
 int mstf_dense_decode_attention(const void* k, const void* v, const int32_t* lengths, int32_t units, int32_t group,
@@ -497,21 +380,16 @@ const char* mstf_status_string(int32_t s) {
 
 int mstf_attention_kernel_count(const mstf_cache* h) {
   if (!h) return MSTF_EINVAL;
-  if (use_r2(h)) return summarize(h, false).uniform ? 2 : 3;  // (+ cost prefix) + attention + combine
-  // register kernel (stream-K) + stream-K combine, or TMA kernel (split grid) + combine
-  return 2;
+  return summarize(h, false).uniform ? 2 : 3;  // (+ cost prefix) + attention + combine
 }
 
-// Dev tooling (declared in include/mustafar.h, "Development only"): the per-CTA timeline of the
-// last attention launch made with MSTF_TRACE set.
-int mstf_dev_trace(void* host, int32_t n) { return copy_trace(host, n) == cudaSuccess ? MSTF_OK : MSTF_ECUDA; }
-
+// Dev tooling (declared in include/mustafar.h, "Development only").
 int mstf_dev_read_bandwidth(const void* src, size_t bytes, void* sink, void* stream) {
   if (!src || !sink || !aligned16(src) || (reinterpret_cast<uintptr_t>(sink) & 3u)) return MSTF_EINVAL;
   return launch_dev_read(src, bytes, static_cast<uint32_t*>(sink), sm_count(), static_cast<cudaStream_t>(stream)) ==
                  cudaSuccess ? MSTF_OK : MSTF_ECUDA;
 }
 
-const char* mstf_build_info(void) { return "mustafar-b200 sm_100a (mma.sync m16n8k16, cp.async.bulk, mbarrier)"; }
+const char* mstf_build_info(void) { return "mustafar-b200 sm_100a (warp-per-worker stream-K, cp.async.bulk + mbarrier, mma.sync m16n8k16, movmatrix)"; }
 
 }  // extern "C"

@@ -104,9 +104,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
-}
 // Gather only when the dibit keeps a channel (mask != 0): idle lanes take no bank slot. The
 // loaded word replaces the address in the same register; a skipped load leaves the address
 // there, which the AND with the (zero) mask clears -- no zeroed register per gather.

@@ -1,5 +1,5 @@
 // compress_dev.cuh -- device code of K1 (per-token magnitude pruning + bitmap compression)
-// shared by compress.cu (prefill / append kernels) and attention.cu (fused decode step).
+// shared by compress.cu (prefill / append kernels) and attn_warp.cu (fused decode step).
 // See compress.cu for the method and its citations.
 #pragma once
 #include <cstdint>

@@ -1,5 +1,5 @@
 // kernels.cuh -- launch interfaces shared between the ABI layer (abi.cu) and the
-// kernels (compress.cu, attention.cu). Not part of the public ABI.
+// kernels (compress.cu, attn_warp.cu, dense.cu). Not part of the public ABI.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -33,13 +33,9 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 
 constexpr int kD = 128;          // head_dim supported by the v1 kernels
 constexpr int kTiles = kD / 64;  // 64-bit bitmap words per token record
-constexpr int kChunk = 64;       // tokens per TMA stage
-constexpr int kConsumerWarps = 4;
+constexpr int kConsumerWarps = 4; // warps per CTA of the dense baseline kernel
 constexpr int kMaxGroup = 8;     // query heads per unit (mma N = 8)
 constexpr int kValuesGuard = 16; // bytes after each VALUES buffer (read past the last record, never used)
-constexpr int kMaxSkGrid = 2 * 148;  // stream-K grid cap (2 CTAs per SM on a B200)
-constexpr int kMaxSkPrefix = 16384;  // ragged stream-K: max units (prefix array in smem)
-constexpr int kSkChunksPerWorker = 2;  // stream-K dynamic tail: at most this many chunks per warp pair
 
 // Device view of one cache (one tensor = K or V shares the same layout).
 struct CacheView {
@@ -63,50 +59,17 @@ cudaError_t launch_query_abs_sum(const uint16_t* q, int32_t U, int32_t R, int32_
 cudaError_t launch_append(const CacheView& c, const uint16_t* k_new, const uint16_t* v_new,
                           cudaStream_t s);
 
-struct AttnPlan {
-  int32_t splits;        // CTAs per unit along the compressed sequence
-  int32_t nstage;        // TMA ring depth
-  int32_t stage_bytes;   // bytes of one stage (K bm, K vals, V bm, V vals for kChunk tokens)
-  int32_t pair_bytes;    // per-CTA shifted pair arrays (4 warps x 16 tokens x K,V)
-  int32_t reg_k, reg_v;  // per-warp region bytes
-  int32_t sk;            // 1: stream-K schedule (register-staged kernel)
-  int32_t sk_static;     // cost units split statically over the workers (warp pairs)
-  int32_t sk_c;          // items per dynamic tail chunk
-  int32_t sk_nchunks;    // dynamic tail chunks
-  int32_t sk_total;      // total items
-  int32_t sk_nb;         // items per unit when all units are equal, else 0
-  int32_t sk_grid;       // CTAs
-};
-// total_items = sum over units of sk_unit_cost(n_comp, W); uniform_items = that per-unit cost
-// when it is the same for every unit, else 0.
-AttnPlan plan_attention(int32_t U, int32_t max_comp, int64_t total_items, int32_t uniform_items,
-                        int32_t kpad_k, int32_t kpad_v, int32_t sm_count);
-bool uses_reg_kernel(int32_t kpad_k, int32_t kpad_v);
-// Stream-K partition cost of one unit (see unit_cost in attention.cu) and its parameters.
+// Stream-K partition cost of one unit (see attn_warp.cu) and its parameters.
 int32_t sk_unit_cost(int32_t n_comp, int32_t W);
 void sk_cost_params(int32_t* cs, int32_t* cw);
-size_t attention_ws_bytes(int32_t U, int32_t G, int32_t max_splits);
-int32_t max_splits_for(int32_t U, int32_t capacity);
-
-// Fused decode step (append + attention in one register-kernel launch; uniform caches only).
-struct FuseArgs {
-  const uint16_t* k_new;
-  const uint16_t* v_new;
-  int32_t nc_old, nw_old;  // counters before the append (same for every unit)
-  int32_t unc, unw;        // after
-  int32_t evict;           // the oldest window token (or, W == 0, the new token) was compressed
-  int32_t epoch;           // stamp of this call's ready flags
-};
-cudaError_t launch_sparse_attention(const CacheView& c, const AttnPlan& plan, int32_t G, const uint16_t* q,
-                                    float scale, void* out, int32_t out_f16, void* ws, cudaStream_t s,
-                                    const FuseArgs* fuse = nullptr, float* part_ml = nullptr,
-                                    float* part_o = nullptr);
 // Sequence split (NEXT-3): partials of an empty shard (m = -inf, l = 0, o = 0), n = U * G.
 cudaError_t launch_empty_partials(float* ml, float* o, int32_t n, cudaStream_t s);
 // Sequence split (NEXT-3): merge n shards' partials [n][U][G] into O [U][G][kD].
 cudaError_t launch_merge_partials(int32_t n, int32_t U, int32_t G, const float* ml, const float* o, void* out,
                                   int32_t out_f16, cudaStream_t s);
 
+// Dense-KV baseline (dense.cu): grid (splits, U) + combine; workspace bytes for `splits`.
+size_t dense_ws_bytes(int32_t U, int32_t G, int32_t splits);
 cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const int32_t* lengths, int32_t U,
                                    int32_t G, int32_t t_max, int32_t splits, const uint16_t* q, float scale,
                                    void* out, int32_t out_f16, void* ws, cudaStream_t s);
@@ -133,7 +96,5 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
 // dev: read-only HBM stream over [src, src + bytes) (bench.py's read-peak measurement)
 cudaError_t launch_dev_read(const void* src, size_t bytes, uint32_t* sink, int sm_count, cudaStream_t s);
 
-// dev: copy the per-CTA timeline recorded when MSTF_TRACE is set (n = 3 * CTAs words)
-cudaError_t copy_trace(void* host, int n);
 
 }  // namespace mstf

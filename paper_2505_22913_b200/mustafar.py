@@ -30,7 +30,7 @@ EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "
            "mstf_dense_decode_attention", "mstf_shard_units", "mstf_decode_step",
            "mstf_decode_step_kernel_count", "mstf_attention_kernel_count",
            "mstf_set_key_weights", "mstf_query_abs_sum",
-           "mstf_seq_split", "mstf_sparse_decode_attention_partial", "mstf_merge_partials", "mstf_dev_trace",
+           "mstf_seq_split", "mstf_sparse_decode_attention_partial", "mstf_merge_partials",
            "mstf_dev_read_bandwidth", "mstf_graph_step_check", "mstf_graph_step_commit",
            "mstf_status_string", "mstf_build_info")
 
@@ -81,7 +81,6 @@ def lib() -> ctypes.CDLL:
         "mstf_seq_split": (ctypes.c_int, [i32, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]),
         "mstf_sparse_decode_attention_partial": (ctypes.c_int, [vp, vp, ctypes.c_float, vp, vp, vp, sz, vp]),
         "mstf_merge_partials": (ctypes.c_int, [i32, i32, i32, i32, vp, vp, vp, i32, vp]),
-        "mstf_dev_trace": (ctypes.c_int, [vp, i32]),
         "mstf_dev_read_bandwidth": (ctypes.c_int, [vp, sz, vp, vp]),
         "mstf_graph_step_check": (ctypes.c_int, [vp, i32]),
         "mstf_graph_step_commit": (ctypes.c_int, [vp, i32]),

@@ -3,7 +3,8 @@
 Runs bench.run_ours (the bench's own timed step, CUDA events, L2-busting layer rotation) for
 the Llama-3-8B attention shape over BASELINE.json's C2 batch range (1..16) at 50% and 70%
 sparsity, and longer contexts at batch 1, and prints one line per point:
-  workload, us per layer-step (append + attention), best dense (torch SDPA / own kernel) us,
+  workload, us per layer-step (append + attention), best dense us (fastest of own kernel, torch
+  SDPA, FlashAttention-2 decode, FlashInfer batch decode),
   sparse/dense speed ratio, roofline frac.
 Usage: python tools/batch_sweep.py [--layers 32]
 """
@@ -26,15 +27,14 @@ def main():
     for b, T, s in pts:
         cfg = dict(desc=f"Llama-3-8B shape, B={b}, T={T}, s={s}", batch=b, hq=32, hkv=8, T=T, sk=s, sv=s,
                    layers=a.layers)
-        args = argparse.Namespace(steps=a.steps, warmup=3, layers=a.layers, dense=True, gather=False,
+        args = argparse.Namespace(steps=a.steps, warmup=3, layers=a.layers, dense=True, gather=False, graph=True,
                                   no_cpu_baseline=True, cpu_seconds=0, workload="sweep")
         r = bench.run_ours(args, cfg, 0, 1, 0)
         d = r["dense_kv"]
         best = d.get("best_dense_us_per_layer")
         step = r["us_per_layer_step"]
         print(json.dumps({"B": b, "T": T, "s": s, "us_per_layer_step": step,
-                          "torch_sdpa_us": round(d.get("torch_sdpa_us_per_layer", 0), 2),
-                          "own_dense_us": round(d.get("own_kernel_us_per_layer", 0), 2),
+                          "best_dense": d.get("best"), "best_dense_us": best,
                           "dense_over_sparse": round(best / step, 3) if best else None,
                           "roofline_frac": r["roofline"]["frac"]}), flush=True)
 
