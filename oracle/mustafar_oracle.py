@@ -29,6 +29,10 @@ What it computes:
     merge_partials      partials and their flash-decoding merge
   * key_scores,         per-token output-aware Key pruning: S = |K| * broadcast(w), top-k of
     prune_tokens_scored S per token, lower index pruned first on ties (R20)
+  * quantize_group,     prune-then-quantize payload ("we first prune each
+    dequantize_group,   token's KV cache before quantization is performed", KIVI 4-bit of
+    compress_tokens_q4  tab:joint_quant): a token's kept values as 4-bit codes with an
+                        asymmetric per-token fp16 scale / zero point (R25-R27)
 
 Pins (tests/test_oracle*.py, `-m "not gpu"`): closed forms, the SPEC worked examples,
 brute-force rank counting and exhaustive subsets on tiny inputs, the lossless round
@@ -47,6 +51,7 @@ __all__ = [
     "compress_tokens", "decompress_tokens", "FormatError", "OracleCache",
     "attention", "attention_dense", "size_model_paper", "size_model_build",
     "query_abs_sum", "key_scores", "prune_tokens_scored", "attention_partial", "merge_partials",
+    "q4_record_bytes", "quantize_group", "dequantize_group", "compress_tokens_q4", "decompress_tokens_q4",
 ]
 
 
@@ -210,6 +215,96 @@ def decompress_tokens(bitmap: np.ndarray, values: np.ndarray, offsets: np.ndarra
     return out
 
 
+# --------------------------------------------------------------------------- 4-bit payload
+def q4_record_bytes(k: int) -> int:
+    """Bytes of one token's quantized payload (R26): fp16 scale, fp16 zero point, ceil(k/2) bytes
+    of 4-bit codes, zero-padded to a multiple of 16 bytes (16-byte aligned records, as R7)."""
+    return ((4 + (k + 1) // 2 + 15) // 16) * 16
+
+
+def quantize_group(vals: np.ndarray):
+    """S:489-490 quantize_group with bits = 4 (KIVI 4-bit; tab:joint_quant): asymmetric
+    uniform mapping, q_max = 15, zero point = min, scale = (max - min) / q_max (1 when that is 0),
+    round half to even. R25 fixes the arithmetic (float32, the kernel's precision, like R20):
+        span  = f32(max) - f32(min)            scale = f16(span / 15), 1.0 if 0 or not finite
+        inv   = 1 / f32(scale)                 code  = rint(min(max((f32(x) - f32(zero)) * inv, 0), 15))
+    every operation rounded to nearest in float32 (rint: half to even); max(NaN, 0) = 0.
+    vals: uint16 fp16 bits [n >= 1] (a token's kept values). Returns (scale bits, zero bits,
+    codes uint8 [n])."""
+    v = np.asarray(vals, dtype=np.uint16).view(np.float16)
+    if v.size == 0:
+        raise ValueError("empty group")
+    lo, hi = v.min(), v.max()
+    span = np.float32(hi) - np.float32(lo)
+    sc = np.float16(np.float32(span) / np.float32(15.0))
+    if not np.isfinite(sc) or sc == 0:
+        sc = np.float16(1.0)
+    inv = np.float32(1.0) / np.float32(sc)
+    with np.errstate(invalid="ignore", over="ignore"):
+        r = (v.astype(np.float32) - np.float32(lo)) * inv
+        q = np.rint(np.fmin(np.fmax(r, np.float32(0)), np.float32(15)))
+    return (np.array(sc, np.float16).view(np.uint16).item(), np.array(lo, np.float16).view(np.uint16).item(),
+            q.astype(np.uint8))
+
+
+def dequantize_group(scale_bits: int, zero_bits: int, codes: np.ndarray) -> np.ndarray:
+    """Inverse map: x = f16(code * scale + zero), the exact value rounded once to fp16 (a
+    correctly rounded fp16 fused multiply-add). Returns uint16 fp16 bits."""
+    sc = float(np.array(scale_bits, np.uint16).view(np.float16))
+    z = float(np.array(zero_bits, np.uint16).view(np.float16))
+    exact = np.asarray(codes, dtype=np.float64) * sc + z        # exact in float64 (15 x 11-bit products)
+    return exact.astype(np.float16).view(np.uint16)
+
+
+def compress_tokens_q4(bits: np.ndarray, keep: np.ndarray, k: int, first_record: int = 0):
+    """Bitmap format with the prune-then-quantize payload: bitmaps and tile
+    offsets exactly as compress_tokens (the selection is unchanged: prune first), and per
+    token one record of q4_record_bytes(k) bytes:
+      [0:2] scale fp16, [2:4] zero fp16, [4 + i//2] code of kept value i (channel order; low nibble
+      for even i), remaining bytes 0x00.
+    Returns (bitmap u64 [T, d/64], records u8 [T, RQ], offsets u32 [T, d/64])."""
+    bits = np.asarray(bits, dtype=np.uint16)
+    keep = np.asarray(keep, dtype=bool)
+    bitmap, values, offsets = compress_tokens(bits, keep, k, first_record)
+    T = bits.shape[0]
+    rq = q4_record_bytes(k)
+    rec = np.zeros((T, rq), dtype=np.uint8)
+    for t in range(T):
+        sc, z, q = quantize_group(values[t, :k])
+        rec[t, 0:2] = np.array([sc], np.uint16).view(np.uint8)
+        rec[t, 2:4] = np.array([z], np.uint16).view(np.uint8)
+        for i, c in enumerate(q):
+            rec[t, 4 + i // 2] |= np.uint8(int(c) << (4 * (i & 1)))
+    return bitmap, rec, offsets
+
+
+def decompress_tokens_q4(bitmap, records, offsets, k: int, d: int, first_record: int = 0) -> np.ndarray:
+    """Dense fp16 bits [T, d] of quantized records: dequantized kept values at the bitmap's
+    positions, exact zeros at pruned channels ("pruned entries remain exact zero"), with
+    validation of the bitmap (popcount k), the offsets, and the record's zero padding."""
+    bitmap = np.asarray(bitmap, dtype=np.uint64)
+    records = np.asarray(records, dtype=np.uint8)
+    T, nt = bitmap.shape
+    rq = q4_record_bytes(k)
+    if records.shape != (T, rq):
+        raise FormatError("record shape")
+    used = 4 + (k + 1) // 2
+    if T and np.any(records[:, used:] != 0):
+        raise FormatError("non-zero record padding")
+    if T and k % 2 and np.any(records[:, 4 + k // 2] >> 4):
+        raise FormatError("non-zero unused nibble")
+    zeros_vals = np.zeros((T, k_pad_of(k)), np.uint16)   # validate bitmaps / offsets only
+    decompress_tokens(bitmap, zeros_vals, offsets, k, d, first_record)
+    keep = np.unpackbits(bitmap.view(np.uint8).reshape(T, nt * 8), axis=-1, bitorder="little").astype(bool)
+    out = np.zeros((T, d), dtype=np.uint16)
+    for t in range(T):
+        sc = int(records[t, 0:2].view(np.uint16)[0])
+        z = int(records[t, 2:4].view(np.uint16)[0])
+        codes = np.array([(records[t, 4 + i // 2] >> (4 * (i & 1))) & 0xF for i in range(k)], np.uint8)
+        out[t, keep[t]] = dequantize_group(sc, z, codes)
+    return out
+
+
 def fp16_to_f64(bits: np.ndarray) -> np.ndarray:
     """Exact fp16 -> float64 (every fp16 value is representable in float64)."""
     return np.asarray(bits, dtype=np.uint16).view(np.float16).astype(np.float64)
@@ -233,15 +328,23 @@ class OracleCache:
     Token p of unit u is compressed into record p (records are in chronological order).
     """
 
-    def __init__(self, U: int, d: int, keep_k: int, keep_v: int, window: int, capacity: int):
+    def __init__(self, U: int, d: int, keep_k: int, keep_v: int, window: int, capacity: int,
+                 value_bits: int = 16):
         self.U, self.d, self.kk, self.kv, self.W, self.cap = U, d, keep_k, keep_v, window, capacity
+        if value_bits not in (16, 4):
+            raise ValueError("value_bits must be 16 or 4")
+        self.value_bits = value_bits   # 4: prune-then-quantize payload (SURVEY NEXT-4, R25-R27)
         self.nt = d // 64
         self.kpk, self.kpv = k_pad_of(keep_k), k_pad_of(keep_v)
         z = np.zeros
         self.bitmap_k = z((U, capacity, self.nt), np.uint64)
         self.bitmap_v = z((U, capacity, self.nt), np.uint64)
-        self.values_k = z((U, capacity, self.kpk), np.uint16)
-        self.values_v = z((U, capacity, self.kpv), np.uint16)
+        if value_bits == 16:
+            self.values_k = z((U, capacity, self.kpk), np.uint16)
+            self.values_v = z((U, capacity, self.kpv), np.uint16)
+        else:   # quantized records [U][cap][q4_record_bytes(k)] bytes
+            self.values_k = z((U, capacity, q4_record_bytes(keep_k)), np.uint8)
+            self.values_v = z((U, capacity, q4_record_bytes(keep_v)), np.uint8)
         self.offsets_k = z((U, capacity, self.nt), np.uint32)
         self.offsets_v = z((U, capacity, self.nt), np.uint32)
         self.win_k = z((U, max(window, 1), d), np.uint16)
@@ -265,7 +368,10 @@ class OracleCache:
             keep = prune_tokens_scored(key_scores(bits, self.key_weights[u]), k)
         else:
             keep = prune_tokens(bits, k)
-        bm, vals, offs = compress_tokens(bits, keep, k, first_record=r0)
+        if self.value_bits == 16:
+            bm, vals, offs = compress_tokens(bits, keep, k, first_record=r0)
+        else:
+            bm, vals, offs = compress_tokens_q4(bits, keep, k, first_record=r0)
         getattr(self, "bitmap_" + which)[u, r0:r0 + len(bits)] = bm
         getattr(self, "values_" + which)[u, r0:r0 + len(bits)] = vals
         getattr(self, "offsets_" + which)[u, r0:r0 + len(bits)] = offs
@@ -312,10 +418,9 @@ class OracleCache:
         """Decompressed K, V of unit u in chronological order (compressed first, then the
         window), as fp16 bit patterns [n, d] -- Alg. 1's K_C, V_C then K_L, V_L."""
         nc, nw = int(self.n_comp[u]), int(self.n_win[u])
-        kc = decompress_tokens(self.bitmap_k[u, :nc], self.values_k[u, :nc], self.offsets_k[u, :nc],
-                               self.kk, self.d)
-        vc = decompress_tokens(self.bitmap_v[u, :nc], self.values_v[u, :nc], self.offsets_v[u, :nc],
-                               self.kv, self.d)
+        dec = decompress_tokens if self.value_bits == 16 else decompress_tokens_q4
+        kc = dec(self.bitmap_k[u, :nc], self.values_k[u, :nc], self.offsets_k[u, :nc], self.kk, self.d)
+        vc = dec(self.bitmap_v[u, :nc], self.values_v[u, :nc], self.offsets_v[u, :nc], self.kv, self.d)
         slots = [(nc + i) % max(self.W, 1) for i in range(nw)]
         kl = self.win_k[u, slots] if nw else np.zeros((0, self.d), np.uint16)
         vl = self.win_v[u, slots] if nw else np.zeros((0, self.d), np.uint16)
