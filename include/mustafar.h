@@ -63,6 +63,11 @@ typedef struct {
   int32_t keep_v;        /* channels kept per Value token, 1..d (K_s != V_s allowed)*/
   int32_t window;        /* dense local window W >= 0 (paper: 32)                    */
   int32_t capacity;      /* max compressed tokens per unit (records per unit)             */
+  int32_t value_bits;    /* payload of the kept values: 16 (or 0) = fp16 values; 4 = the
+                            prune-then-quantize payload ("we first
+                            prune each token's KV cache before quantization is performed",
+                            KIVI 4-bit of tab:joint_quant): per token 4-bit codes with an fp16
+                            scale and zero point over its kept values (R25-R27)              */
 } mstf_config;
 
 /* k = d - floor(s*d) for s in [0,1) (R1). Returns MSTF_EKEEP for s outside. */
@@ -70,6 +75,10 @@ int32_t mstf_keep_from_sparsity(double sparsity, int32_t head_dim);
 
 /* Packed-value slots per token: ceil(k/8)*8 ("multiples-of-8 padding"; R7). */
 int32_t mstf_k_pad(int32_t keep);
+
+/* Bytes of one token's value record: 2 * mstf_k_pad(keep) for value_bits 16 (or 0);
+ * for value_bits 4, round_up(4 + ceil(keep / 2), 16) (R26). MSTF_EINVAL for other value_bits. */
+int32_t mstf_value_record_bytes(int32_t keep, int32_t value_bits);
 
 /* ------------------------------------------------------------------ cache buffers
  * The compressed format ("compressed tiles corresponding to a 1x64 column of the
@@ -81,9 +90,12 @@ int32_t mstf_k_pad(int32_t keep);
  *                                       exactly keep_x bits set per record (R4)
  *   VALUES_x  u16 [U][capacity][kpad]   kept fp16 bit patterns in ascending channel order,
  *                                       then 0x0000 up to kpad = mstf_k_pad(keep_x) (R6, R7);
- *                                       the buffer is 16 bytes longer (tail guard: the
- *                                       attention kernels read, never use, up to 8 bytes
- *                                       past the last record)
+ *                                       the buffer is 16 bytes longer (tail guard);
+ *             value_bits 4: u8 [U][capacity][rq], rq = mstf_value_record_bytes(keep_x, 4):
+ *                                       bytes 0-1 scale (fp16), 2-3 zero point (fp16), byte 4 + i/2
+ *                                       the 4-bit code of kept value i (channel order, low nibble
+ *                                       for even i), then 0x00 padding; value i reconstructs to
+ *                                       f16(code_i * scale + zero) (R25-R27)
  *   OFFSETS_x u32 [U][capacity][d/64]   p*kpad + (kept channels in tiles < j): element index
  *                                       of tile j's first value in the unit's value array (R8)
  *   WIN_x     u16 [U][max(W,1)][d]      dense window ring: token p sits in slot p % W (R9)

@@ -231,10 +231,16 @@ def quantize_group(vals: np.ndarray):
     every operation rounded to nearest in float32 (rint: half to even); max(NaN, 0) = 0.
     vals: uint16 fp16 bits [n >= 1] (a token's kept values). Returns (scale bits, zero bits,
     codes uint8 [n])."""
-    v = np.asarray(vals, dtype=np.uint16).view(np.float16)
-    if v.size == 0:
+    b = np.asarray(vals, dtype=np.uint16)
+    if b.size == 0:
         raise ValueError("empty group")
-    lo, hi = v.min(), v.max()
+    if not np.all(np.isfinite(b.view(np.float16))):
+        raise ValueError("non-finite input (S:491)")
+    v = b.view(np.float16)
+    # min / max in the total order of fp16 values with -0 < +0 (R25: the zero point's sign is
+    # well defined when both zeros are kept): order key = bits ^ 0x8000 for x >= +0, ~bits else
+    key = np.where(b & 0x8000, (~b) & 0xFFFF, b | 0x8000).astype(np.int64)
+    lo, hi = v[np.argmin(key)], v[np.argmax(key)]
     span = np.float32(hi) - np.float32(lo)
     sc = np.float16(np.float32(span) / np.float32(15.0))
     if not np.isfinite(sc) or sc == 0:

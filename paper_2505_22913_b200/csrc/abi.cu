@@ -28,6 +28,7 @@ int validate(const mstf_config* c) {
     return MSTF_EINVAL;
   if (c->head_dim % 64 != 0 || c->num_q_heads % c->num_kv_heads != 0) return MSTF_ESHAPE;
   if (c->keep_k < 1 || c->keep_k > c->head_dim || c->keep_v < 1 || c->keep_v > c->head_dim) return MSTF_EKEEP;
+  if (c->value_bits != 0 && c->value_bits != 16 && c->value_bits != 4) return MSTF_EINVAL;
   if (c->head_dim != kD || c->num_q_heads / c->num_kv_heads > kMaxGroup) return MSTF_ENOTSUP;
   return MSTF_OK;
 }
@@ -61,6 +62,13 @@ int32_t mstf_keep_from_sparsity(double s, int32_t d) {
 
 int32_t mstf_k_pad(int32_t keep) { return ((keep + 7) / 8) * 8; }
 
+int32_t mstf_value_record_bytes(int32_t keep, int32_t value_bits) {
+  if (keep < 1) return MSTF_EKEEP;
+  if (value_bits == 0 || value_bits == 16) return 2 * mstf_k_pad(keep);
+  if (value_bits == 4) return ((4 + (keep + 1) / 2 + 15) / 16) * 16;
+  return MSTF_EINVAL;
+}
+
 int mstf_cache_buffer_bytes(const mstf_config* c, size_t sizes[MSTF_NUM_BUFFERS]) {
   const int st = validate(c);
   if (st != MSTF_OK && st != MSTF_ENOTSUP) return st;
@@ -69,8 +77,8 @@ int mstf_cache_buffer_bytes(const mstf_config* c, size_t sizes[MSTF_NUM_BUFFERS]
   const size_t W = c->window > 0 ? c->window : 1;
   sizes[MSTF_BUF_BITMAP_K] = sizes[MSTF_BUF_BITMAP_V] = U * cap * nt * 8;
   // + kValuesGuard: the attention kernels' per-token loads may read up to 8 bytes past a record
-  sizes[MSTF_BUF_VALUES_K] = U * cap * mstf_k_pad(c->keep_k) * 2 + kValuesGuard;
-  sizes[MSTF_BUF_VALUES_V] = U * cap * mstf_k_pad(c->keep_v) * 2 + kValuesGuard;
+  sizes[MSTF_BUF_VALUES_K] = U * cap * (size_t)mstf_value_record_bytes(c->keep_k, c->value_bits) + kValuesGuard;
+  sizes[MSTF_BUF_VALUES_V] = U * cap * (size_t)mstf_value_record_bytes(c->keep_v, c->value_bits) + kValuesGuard;
   sizes[MSTF_BUF_OFFSETS_K] = sizes[MSTF_BUF_OFFSETS_V] = U * cap * nt * 4;
   sizes[MSTF_BUF_WIN_K] = sizes[MSTF_BUF_WIN_V] = U * W * c->head_dim * 2;
   sizes[MSTF_BUF_N_COMP] = sizes[MSTF_BUF_N_WIN] = U * 4;
@@ -102,6 +110,9 @@ int mstf_cache_create(const mstf_config* c, void* const buffers[MSTF_NUM_BUFFERS
   v.keep[1] = c->keep_v;
   v.kpad[0] = mstf_k_pad(c->keep_k);
   v.kpad[1] = mstf_k_pad(c->keep_v);
+  v.vbits = c->value_bits == 4 ? 4 : 16;
+  v.rq[0] = mstf_value_record_bytes(c->keep_k, c->value_bits);
+  v.rq[1] = mstf_value_record_bytes(c->keep_v, c->value_bits);
   h->nc.assign(v.U, 0);
   h->nw.assign(v.U, 0);
   *out = h;
@@ -192,7 +203,8 @@ int launch_attention(const mstf_cache* h, const MirrorSummary& ms, bool fuse, co
               const void* q, float scale, void* out, int32_t out_dtype, float* part_ml, float* part_o, void* ws,
               void* stream) {
   const int32_t G = h->cfg.num_q_heads / h->cfg.num_kv_heads;
-  const WarpPlan plan = plan_warp_attention(h->view.U, G, ms.total_cost, h->view.kpad[0], h->view.kpad[1], sm_count());
+  const WarpPlan plan = plan_warp_attention(h->view.U, G, ms.total_cost, h->view.kpad[0], h->view.kpad[1],
+                                            h->view.rq[0], h->view.rq[1], sm_count());
   const cudaError_t e = launch_warp_attention(
       h->view, plan, G, ms.uniform ? 1 : 0, fuse ? 1 : 0, static_cast<const uint16_t*>(q), scale,
       static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), out, out_dtype == MSTF_OUT_F16,

@@ -60,6 +60,7 @@ struct WParams {
   int uniform;            // every unit has the same counters (closed-form partition)
   int fuse;               // append inside (uniform caches only)
   int kpk, kpv;           // k_pad of K and V
+  int rqk, rqv;           // bytes of one token's value record (2 k_pad, or the 4-bit record)
   int stage_bytes, off_kval, off_vbm, off_vval;
   int swk, swv;           // pair-array stride per token (32-bit words)
   int warp_bytes;         // per-warp shared-memory region
@@ -219,6 +220,51 @@ __device__ __forceinline__ void build_token(uint32_t raw, uint32_t ydst, int nch
   sts32(ydst + 32u * nch, prmt(prev, 0u, 0x5432));
 }
 
+// The same pair arrays from a 4-bit record: [scale f16][zero f16][codes,
+// low nibble first]. Each pair of codes becomes fp16 integers through the 1024 + c bit trick
+// (exact), then one fp16 FMA per pair reconstructs f16(c * scale + zero) -- the oracle's single
+// rounding. nch = kp / 8 code words (8 codes each; codes past k reconstruct to `zero`, which no
+// unmasked gather reads).
+__device__ __forceinline__ uint32_t hsub2_u(uint32_t a, uint32_t b) {
+  __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) {
+  __half2 r = __hfma2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b), *reinterpret_cast<__half2*>(&c));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+template <int NCH>
+__device__ __forceinline__ void build_token_q4(uint32_t rec, uint32_t ydst, int nch_rt) {
+  const int nch = NCH ? NCH : nch_rt;
+  const uint32_t sz = lds32(rec);
+  const uint32_t sc2 = prmt(sz, 0u, 0x1010), z2 = prmt(sz, 0u, 0x3232);
+  uint32_t prev = 0;
+  sts32(ydst, 0u);
+#pragma unroll
+  for (int c = 0; c < (NCH ? NCH : 16); ++c) {
+    if (!NCH && c >= nch) break;
+    const uint32_t w = lds32(rec + 4 + 4 * c);
+    const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
+    uint32_t R[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t t = (prmt(lo, hi, (uint32_t)(((4 + i) << 8) | i)) & 0x00FF00FFu) | 0x64006400u;
+      R[i] = hfma2_u(hsub2_u(t, 0x64006400u), sc2, z2);
+    }
+    const uint32_t d = ydst + 32u * c;
+    sts32(d, prmt(prev, R[0], 0x5432));
+    sts32(d + 4, R[0]);
+    sts32(d + 8, prmt(R[0], R[1], 0x5432));
+    sts32(d + 12, R[1]);
+    sts32(d + 16, prmt(R[1], R[2], 0x5432));
+    sts32(d + 20, R[2]);
+    sts32(d + 24, prmt(R[2], R[3], 0x5432));
+    sts32(d + 28, R[3]);
+    prev = R[3];
+  }
+  sts32(ydst + 32u * nch, prmt(prev, 0u, 0x5432));
+}
+
 // ---------------------------------------------------------------- schedule (device side)
 // Cost model of the partition (same as the r1 stream-K schedule): a unit's cost list is
 // [cs start units][one per compressed 16-token block][cw per window block]; worker P owns
@@ -271,7 +317,7 @@ __device__ __forceinline__ void wait_ready(const int* flag) {
 
 // ---------------------------------------------------------------- the kernel
 // G = 8 holds twice the accumulators and q fragments: at most 8 warps per CTA (<= 255 registers).
-template <int NK, int NV, bool G8>
+template <int NK, int NV, bool G8, bool Q4>
 __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mstf_attn_warp_kernel(const WParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -349,8 +395,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     const size_t rec = (size_t)pu * c.cap + (size_t)pb * 16;
     g_kbm = reinterpret_cast<const uint8_t*>(c.bm[0]) + rec * 16;
     g_vbm = reinterpret_cast<const uint8_t*>(c.bm[1]) + rec * 16;
-    g_kv = reinterpret_cast<const uint8_t*>(c.val[0]) + rec * 2 * p.kpk;
-    g_vv = reinterpret_cast<const uint8_t*>(c.val[1]) + rec * 2 * p.kpv;
+    g_kv = reinterpret_cast<const uint8_t*>(c.val[0]) + rec * p.rqk;
+    g_vv = reinterpret_cast<const uint8_t*>(c.val[1]) + rec * p.rqv;
   };
   p_unit();
   // advance the producer to its next compressed block (or done)
@@ -358,8 +404,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     ++pb;
     g_kbm += 256;
     g_vbm += 256;
-    g_kv += 32 * p.kpk;
-    g_vv += 32 * p.kpv;
+    g_kv += 16 * p.rqk;
+    g_vv += 16 * p.rqv;
     while (!pdone && pb >= pbe) {
       ++pu;
       if (pu >= c.U || unit_start(p, pu, cpu) >= x1) { pdone = true; break; }
@@ -375,7 +421,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     }
     const int s = pseq & (kWNst - 1);
     const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes), bar = bar0 + 8 * s;
-    const uint32_t bytes_bm = n * 16, bytes_k = n * 2 * p.kpk, bytes_v = n * 2 * p.kpv;
+    const uint32_t bytes_bm = n * 16, bytes_k = n * p.rqk, bytes_v = n * p.rqv;
     mbar_expect_tx_u32(bar, 2 * bytes_bm + bytes_k + bytes_v);
     bulk_g2s_u32(st, g_kbm, bytes_bm, bar);
     bulk_g2s_u32(st + p.off_kval, g_kv, bytes_k, bar);
@@ -405,8 +451,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   const uint32_t par = (uint32_t)(g >> 2);
   const uint32_t sel_lo = par ? 0x1044u : 0x4410u, sel_hi = par ? 0x3244u : 0x4432u;
   // build role of this lane: token lane & 15 of K (lanes 0-15) or V (16-31)
-  const uint32_t raw_off = lane < 16 ? (uint32_t)(p.off_kval + (lane & 15) * 2 * p.kpk)
-                                     : (uint32_t)(p.off_vval + (lane & 15) * 2 * p.kpv);
+  const uint32_t raw_off = lane < 16 ? (uint32_t)(p.off_kval + (lane & 15) * p.rqk)
+                                     : (uint32_t)(p.off_vval + (lane & 15) * p.rqv);
   const uint32_t ydst = lane < 16 ? ypk + 4u * (uint32_t)((lane & 15) * p.swk) : ypv + 4u * (uint32_t)((lane & 15) * p.swv);
   const int nch_me = (lane < 16 ? p.kpk : p.kpv) >> 3;
   int qu = -1;
@@ -531,7 +577,10 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes);
       mbar_wait_u32(bar0 + 8 * s, (uint32_t)(cseq / kWNst) & 1u);
       const int nvalid = min(16, cn.nc - b * 16);
-      build_token<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
+      if constexpr (Q4)
+        build_token_q4<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
+      else
+        build_token<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
       // K bitmap word t of tokens g, g + 8; V half-word g of tokens 2t, 2t+1, 8+2t, 9+2t
       const uint32_t kw0 = g < nvalid ? lds32(st + 16 * g + 4 * t) : 0u;
       const uint32_t kw1 = g + 8 < nvalid ? lds32(st + 16 * (g + 8) + 4 * t) : 0u;
@@ -827,9 +876,9 @@ __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p)
   }
 }
 
-template <int NK, int NV>
+template <int NK, int NV, bool Q4 = false>
 void* pick_kernel(bool g8) {
-  return g8 ? (void*)mstf_attn_warp_kernel<NK, NV, true> : (void*)mstf_attn_warp_kernel<NK, NV, false>;
+  return g8 ? (void*)mstf_attn_warp_kernel<NK, NV, true, Q4> : (void*)mstf_attn_warp_kernel<NK, NV, false, Q4>;
 }
 
 }  // namespace
@@ -869,16 +918,17 @@ bool warp_kernel_supported(int32_t G) { return G >= 1 && G <= 8; }
 
 static int pair_sw(int kp) { return kp + 2; }  // words per token: Y[0..kp]; 2 mod 4 (conflict-free build)
 
-int warp_region_bytes(int32_t kpk, int32_t kpv, int* stage_bytes) {
-  const int st = 16 * (16 + 2 * kpk) + 16 * (16 + 2 * kpv);
+int warp_region_bytes(int32_t kpk, int32_t kpv, int32_t rqk, int32_t rqv, int* stage_bytes) {
+  const int st = 16 * (16 + rqk) + 16 * (16 + rqv);
   if (stage_bytes) *stage_bytes = st;
   const int pairs = (64 * pair_sw(kpk) + 127) / 128 * 128 + 4 + 64 * pair_sw(kpv);
   return (kWNst * st + (pairs + 7) / 8 * 8 + 8 * kWNst + 127) / 128 * 128;
 }
 
-WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t sm_count) {
+WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t rqk,
+                             int32_t rqv, int32_t sm_count) {
   WarpPlan pl;
-  const int wb = warp_region_bytes(kpk, kpv, nullptr);
+  const int wb = warp_region_bytes(kpk, kpv, rqk, rqv, nullptr);
   int wmax = (int)((227 * 1024) / wb);
   const int wcap = G > 4 ? kWMaxWarps / 2 : kWMaxWarps;
   if (wmax > wcap) wmax = wcap;
@@ -921,10 +971,12 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   p.fuse = fuse;
   p.kpk = c.kpad[0];
   p.kpv = c.kpad[1];
+  p.rqk = c.rq[0];
+  p.rqv = c.rq[1];
   p.stage_bytes = 0;
-  p.warp_bytes = warp_region_bytes(p.kpk, p.kpv, &p.stage_bytes);
+  p.warp_bytes = warp_region_bytes(p.kpk, p.kpv, p.rqk, p.rqv, &p.stage_bytes);
   p.off_kval = 256;
-  p.off_vbm = p.off_kval + 32 * p.kpk;
+  p.off_vbm = p.off_kval + 16 * p.rqk;
   p.off_vval = p.off_vbm + 256;
   p.swk = pair_sw(p.kpk);
   p.swv = pair_sw(p.kpv);
@@ -954,7 +1006,8 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   const bool g8 = G > 4;
   void* kern = nullptr;
   const int nk = c.kpad[0] / 8, nv = c.kpad[1] / 8;
-  if (nk == nv && nk == 5) kern = pick_kernel<5, 5>(g8);
+  if (c.vbits == 4) kern = pick_kernel<0, 0, true>(g8);
+  else if (nk == nv && nk == 5) kern = pick_kernel<5, 5>(g8);
   else if (nk == nv && nk == 8) kern = pick_kernel<8, 8>(g8);
   else if (nk == nv && nk == 4) kern = pick_kernel<4, 4>(g8);
   else if (nk == nv && nk == 2) kern = pick_kernel<2, 2>(g8);

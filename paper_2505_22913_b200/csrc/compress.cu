@@ -67,16 +67,17 @@ __global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint
     const Sel z = sel_tensor(c, x);
     const uint32_t kk = (uint32_t)z.keep;
     const int gend = min(g0 + 4 * kPrefillGroups, ntok);
-    if (x == 0 && c.kw) {
-      // output-aware K pruning: one warp per token, float32 score keys
-      const float* kw = c.kw + (size_t)u * kD;
-      const uint16_t* base = k + (size_t)u * T * kD;
+    if ((x == 0 && c.kw) || c.vbits == 4) {
+      // output-aware K pruning (float32 score keys) or the 4-bit payload (NEXT-4): one
+      // warp per token
+      const float* kw = (x == 0 && c.kw) ? c.kw + (size_t)u * kD : nullptr;
+      const uint16_t* base = (x ? v : k) + (size_t)u * T * kD;
       for (int t = g0; t < gend; ++t) {
         const uint2 raw = reinterpret_cast<const uint2*>(base + (size_t)t * kD)[lane];
         if (t < nc) {
           const size_t rec = (size_t)u * c.cap + t;
-          compress_raw_warp(raw, z.keep, z.kpad, (uint32_t)t, z.bm + rec * kTiles, z.val + rec * z.kpad,
-                            z.off + rec * kTiles, lane, kw);
+          compress_raw_warp(raw, z.keep, z.kpad, (uint32_t)t, z.bm + rec * kTiles, z.rec_val(rec),
+                            z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
         } else {
           reinterpret_cast<uint2*>(z.win + ((size_t)u * c.W + (t % c.W)) * kD)[lane] = raw;
         }

@@ -117,13 +117,78 @@ __device__ __forceinline__ uint32_t select_keep_nibble_scored(uint32_t x, uint32
   return keep_nibble_at(m, tau, k);
 }
 
+// Order key of an fp16 bit pattern: unsigned order == value order, with -0 < +0 (R25).
+__device__ __forceinline__ uint32_t f16_order_key(uint32_t h) { return (h & 0x8000u) ? (~h & 0xFFFFu) : (h | 0x8000u); }
+__device__ __forceinline__ uint32_t f16_from_key(uint32_t k) { return (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu); }
+__device__ __forceinline__ uint32_t warp_min(uint32_t x) {
+  uint32_t r;
+  asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t warp_max(uint32_t x) {
+  uint32_t r;
+  asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(x));
+  return r;
+}
+
+// 4-bit payload of one token: lane l holds the fp16 values h[4] of
+// channels 4l..4l+3, keep nibble nib, and pos = kept channels of lower lanes. Writes the record
+// [scale f16][zero f16][k nibbles, kept order, low nibble first][zero padding to rq bytes]:
+// zero = least kept value (-0 < +0), scale = f16(f32(max - min) / 15) (1 if 0), code =
+// rint(clamp((f32(x) - f32(zero)) * (1 / f32(scale)), 0, 15)), float32 round-to-nearest.
+__device__ __forceinline__ void quantize_token_warp(const uint32_t (&h)[4], uint32_t nib, uint32_t pos, int k, int rq,
+                                                    uint8_t* __restrict__ rec_out, int lane) {
+  uint32_t kmin = 0xFFFFu, kmax = 0u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t key = f16_order_key(h[j]);
+    if (nib & (1u << j)) {
+      kmin = min(kmin, key);
+      kmax = max(kmax, key);
+    }
+  }
+  kmin = warp_min(kmin);
+  kmax = warp_max(kmax);
+  const uint32_t zero_bits = f16_from_key(kmin), max_bits = f16_from_key(kmax);
+  const float lo = __half2float(__ushort_as_half((unsigned short)zero_bits));
+  const float hi = __half2float(__ushort_as_half((unsigned short)max_bits));
+  __half sc = __float2half_rn(__fdiv_rn(__fsub_rn(hi, lo), 15.f));
+  const float scf = __half2float(sc);
+  if (!(scf != 0.f && isfinite(scf))) sc = __float2half_rn(1.f);
+  const float inv = __frcp_rn(__half2float(sc));
+  // this lane's codes in kept order as a nibble string, placed at nibble pos of the token
+  uint32_t str = 0, n = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (nib & (1u << j)) {
+      const float x = __half2float(__ushort_as_half((unsigned short)h[j]));
+      const float r = fminf(fmaxf(__fmul_rn(__fsub_rn(x, lo), inv), 0.f), 15.f);
+      str |= (uint32_t)rintf(r) << (4 * n);
+      ++n;
+    }
+  }
+  const unsigned long long placed = (unsigned long long)str << (4 * (pos & 7u));
+  const uint32_t w0 = pos >> 3;
+  const int ncw = (k + 7) >> 3;  // code words
+  uint32_t mine = 0;             // record word lane (0: scale | zero, 1..: codes, rest: padding)
+  for (int wi = 0; wi < ncw; ++wi) {
+    const uint32_t part = (w0 == (uint32_t)wi ? (uint32_t)placed : 0u) | (w0 + 1 == (uint32_t)wi ? (uint32_t)(placed >> 32) : 0u);
+    const uint32_t word = warp_or(part);
+    if (lane == wi + 1) mine = word;
+  }
+  if (lane == 0) mine = (uint32_t)__half_as_ushort(sc) | (zero_bits << 16);
+  if (lane < rq / 4) reinterpret_cast<uint32_t*>(rec_out)[lane] = mine;
+}
+
 // Compress one fp16 token vector (raw = this lane's 4 channels, already loaded) into record
-// `rec` (a3): bitmaps, packed values + zero padding, tile offsets.
+// `rec` (a3): bitmaps, packed values + zero padding (or the 4-bit record when vbits == 4),
+// tile offsets.
 // kw: this unit's float32 channel weights for output-aware K pruning, or null (magnitude).
 __device__ __forceinline__ void compress_raw_warp(uint2 raw, int k, int kpad, uint32_t rec,
                                                   uint64_t* __restrict__ bm_out, uint16_t* __restrict__ val_out,
                                                   uint32_t* __restrict__ off_out, int lane,
-                                                  const float* __restrict__ kw = nullptr) {
+                                                  const float* __restrict__ kw = nullptr, int vbits = 16,
+                                                  int rq = 0) {
   const uint32_t nib = kw ? select_keep_nibble_scored(raw.x, raw.y, reinterpret_cast<const float4*>(kw)[lane], (uint32_t)k)
                           : select_keep_nibble(raw.x, raw.y, (uint32_t)k, lane);
   // 128-bit keep mask: word i = channels 32i..32i+31 = lanes 8i..8i+7
@@ -136,11 +201,16 @@ __device__ __forceinline__ void compress_raw_warp(uint2 raw, int k, int kpad, ui
 #pragma unroll
   for (int i = 0; i < 3; ++i) pos += (i < wi) ? __popc(w[i]) : 0u;
   const uint32_t h[4] = {raw.x & 0xFFFFu, raw.x >> 16, raw.y & 0xFFFFu, raw.y >> 16};
+  if (vbits == 4) {
+    quantize_token_warp(h, nib, pos, k, rq, reinterpret_cast<uint8_t*>(val_out), lane);
+  } else {
+    uint32_t p = pos;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (nib & (1u << j)) val_out[pos++] = (uint16_t)h[j];
+    for (int j = 0; j < 4; ++j) {
+      if (nib & (1u << j)) val_out[p++] = (uint16_t)h[j];
+    }
+    if (lane < kpad - k) val_out[k + lane] = 0;  // zero padding
   }
-  if (lane < kpad - k) val_out[k + lane] = 0;  // zero padding
   if (lane == 0) {
     *reinterpret_cast<uint4*>(bm_out) = make_uint4(w[0], w[1], w[2], w[3]);  // tile0 = w0 | w1 << 32
     const uint32_t base = rec * (uint32_t)kpad;
@@ -153,9 +223,10 @@ __device__ __forceinline__ void compress_token_warp(const uint16_t* __restrict__
                                                     uint32_t rec, uint64_t* __restrict__ bm_out,
                                                     uint16_t* __restrict__ val_out,
                                                     uint32_t* __restrict__ off_out, int lane,
-                                                    const float* __restrict__ kw = nullptr) {
+                                                    const float* __restrict__ kw = nullptr, int vbits = 16,
+                                                    int rq = 0) {
   const uint2 raw = *reinterpret_cast<const uint2*>(src + 4 * lane);
-  compress_raw_warp(raw, k, kpad, rec, bm_out, val_out, off_out, lane, kw);
+  compress_raw_warp(raw, k, kpad, rec, bm_out, val_out, off_out, lane, kw, vbits, rq);
 }
 
 __device__ __forceinline__ void copy_token_warp(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
@@ -164,7 +235,11 @@ __device__ __forceinline__ void copy_token_warp(const uint16_t* __restrict__ src
 }
 
 struct Sel {
-  uint64_t* bm; uint16_t* val; uint32_t* off; uint16_t* win; int keep, kpad;
+  uint64_t* bm; uint16_t* val; uint32_t* off; uint16_t* win; int keep, kpad, rq;
+  // value record of record index rec (fp16 values or the 4-bit record)
+  __device__ __forceinline__ uint16_t* rec_val(size_t rec) const {
+    return reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(val) + rec * (size_t)rq);
+  }
 };
 __device__ __forceinline__ Sel sel_tensor(const CacheView& c, int x) {
   Sel r;
@@ -174,6 +249,7 @@ __device__ __forceinline__ Sel sel_tensor(const CacheView& c, int x) {
   r.win = x ? c.win[1] : c.win[0];
   r.keep = x ? c.keep[1] : c.keep[0];
   r.kpad = x ? c.kpad[1] : c.kpad[0];
+  r.rq = x ? c.rq[1] : c.rq[0];
   return r;
 }
 
@@ -187,12 +263,12 @@ __device__ __forceinline__ void append_unit_warp(const CacheView& c, int x, int 
   const Sel z = sel_tensor(c, x);
   const float* kw = (x == 0 && c.kw) ? c.kw + (size_t)u * kD : nullptr;
   if (c.W == 0) {
-    compress_token_warp(src, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.val + rec * z.kpad,
-                        z.off + rec * kTiles, lane, kw);
+    compress_token_warp(src, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.rec_val(rec),
+                        z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
   } else if (nw == c.W) {
     uint16_t* slot = z.win + ((size_t)u * c.W + (nc % c.W)) * kD;
-    compress_token_warp(slot, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.val + rec * z.kpad,
-                        z.off + rec * kTiles, lane, kw);
+    compress_token_warp(slot, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.rec_val(rec),
+                        z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
     __syncwarp();
     copy_token_warp(src, slot, lane);
   } else {

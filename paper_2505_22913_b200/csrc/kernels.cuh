@@ -40,13 +40,15 @@ constexpr int kValuesGuard = 16; // bytes after each VALUES buffer (read past th
 // Device view of one cache (one tensor = K or V shares the same layout).
 struct CacheView {
   uint64_t* bm[2];      // [U][cap][kTiles]
-  uint16_t* val[2];     // [U][cap][kpad]
+  uint16_t* val[2];     // [U][cap][kpad] fp16 values, or [U][cap][rq] bytes (4-bit payload)
   uint32_t* off[2];     // [U][cap][kTiles]
   uint16_t* win[2];     // [U][max(W,1)][kD]
   int32_t* n_comp;      // [U]
   int32_t* n_win;       // [U]
   int32_t U, W, cap;
   int32_t keep[2], kpad[2];
+  int32_t vbits;        // 16: fp16 values; 4: quantized records (NEXT-4)
+  int32_t rq[2];        // bytes of one token's value record: 2*kpad (fp16) or the 4-bit record
   const float* kw;      // [U][kD] float32 K channel weights (output-aware pruning), or null
 };
 
@@ -84,8 +86,9 @@ struct WarpPlan {
 };
 bool warp_kernel_supported(int32_t G);
 size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count);
-int warp_region_bytes(int32_t kpk, int32_t kpv, int* stage_bytes);
-WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t sm_count);
+int warp_region_bytes(int32_t kpk, int32_t kpv, int32_t rqk, int32_t rqv, int* stage_bytes);
+WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t rqk,
+                             int32_t rqv, int32_t sm_count);
 // uniform: every unit has the same counters (fuse requires it). fuse: k_new / v_new are appended
 // inside the launch (the counters are then advanced by the combine kernel).
 cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int32_t G, int32_t uniform, int32_t fuse,

@@ -24,7 +24,7 @@ BUFFERS = ("bitmap_k", "bitmap_v", "values_k", "values_v", "offsets_k", "offsets
            "win_k", "win_v", "n_comp", "n_win")
 NUM_BUFFERS = len(BUFFERS)
 OUT_F32, OUT_F16 = 0, 1
-EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_cache_buffer_bytes", "mstf_cache_create",
+EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_value_record_bytes", "mstf_cache_buffer_bytes", "mstf_cache_create",
            "mstf_cache_destroy", "mstf_cache_counts", "mstf_prune_compress_kv", "mstf_append_token",
            "mstf_workspace_bytes", "mstf_sparse_decode_attention", "mstf_dense_workspace_bytes",
            "mstf_dense_decode_attention", "mstf_shard_units", "mstf_decode_step",
@@ -43,7 +43,8 @@ class MustafarError(RuntimeError):
 
 class Config(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("batch", "num_q_heads", "num_kv_heads", "head_dim", "keep_k", "keep_v", "window", "capacity")]
+                ("batch", "num_q_heads", "num_kv_heads", "head_dim", "keep_k", "keep_v", "window", "capacity",
+                 "value_bits")]
 
 
 _lib = None
@@ -61,6 +62,7 @@ def lib() -> ctypes.CDLL:
     sig = {
         "mstf_keep_from_sparsity": (i32, [ctypes.c_double, i32]),
         "mstf_k_pad": (i32, [i32]),
+        "mstf_value_record_bytes": (i32, [i32, i32]),
         "mstf_cache_buffer_bytes": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.POINTER(sz)]),
         "mstf_cache_create": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.POINTER(vp), ctypes.POINTER(vp)]),
         "mstf_cache_destroy": (ctypes.c_int, [vp]),
@@ -205,8 +207,9 @@ class MustafarCache:
     """One compressed KV cache (one layer, all (batch, kv-head) units) on one device."""
 
     def __init__(self, batch, num_q_heads, num_kv_heads, head_dim, keep_k, keep_v, window, capacity,
-                 device=None):
-        self.cfg = Config(batch, num_q_heads, num_kv_heads, head_dim, keep_k, keep_v, window, capacity)
+                 device=None, value_bits=16):
+        self.cfg = Config(batch, num_q_heads, num_kv_heads, head_dim, keep_k, keep_v, window, capacity, value_bits)
+        self.value_bits = value_bits
         self.shape = Shape(batch, num_q_heads, num_kv_heads, head_dim)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         sizes = buffer_bytes(self.cfg)
@@ -251,8 +254,8 @@ class MustafarCache:
             "bitmap_k": r["bitmap_k"].view(torch.int64).view(U, cap, nt),
             "bitmap_v": r["bitmap_v"].view(torch.int64).view(U, cap, nt),
             # the values buffers end with a 16-byte tail guard (include/mustafar.h)
-            "values_k": r["values_k"][:U * cap * k_pad(self.keep_k) * 2].view(torch.int16).view(U, cap, k_pad(self.keep_k)),
-            "values_v": r["values_v"][:U * cap * k_pad(self.keep_v) * 2].view(torch.int16).view(U, cap, k_pad(self.keep_v)),
+            "values_k": self._values_view(r["values_k"], self.keep_k),
+            "values_v": self._values_view(r["values_v"], self.keep_v),
             "offsets_k": r["offsets_k"].view(torch.int32).view(U, cap, nt),
             "offsets_v": r["offsets_v"].view(torch.int32).view(U, cap, nt),
             "win_k": r["win_k"].view(torch.int16).view(U, W, d),
@@ -260,6 +263,13 @@ class MustafarCache:
             "n_comp": r["n_comp"].view(torch.int32),
             "n_win": r["n_win"].view(torch.int32),
         }
+
+    def _values_view(self, raw, keep):
+        U, cap = self.units, self.capacity
+        rq = int(lib().mstf_value_record_bytes(int(keep), int(self.value_bits)))
+        if self.value_bits == 4:  # 4-bit records [U][cap][rq] bytes
+            return raw[:U * cap * rq].view(U, cap, rq)
+        return raw[:U * cap * rq].view(torch.int16).view(U, cap, rq // 2)
 
     def attention_kernel_count(self) -> int:
         """Kernels launched by one sparse_decode_attention call on this cache."""

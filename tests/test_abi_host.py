@@ -47,9 +47,23 @@ def test_keep_and_pad(L):
     assert [L.mstf_k_pad(k) for k in (1, 8, 9, 39, 64, 128)] == [8, 8, 16, 40, 64, 128]
 
 
+def test_value_record_bytes(L):
+    """R7 / R26: fp16 records are 2 * k_pad bytes; 4-bit records round_up(4 + ceil(k/2), 16)
+    (the oracle's q4_record_bytes); any other width is rejected."""
+    from oracle import mustafar_oracle as O
+    for k in (1, 13, 39, 64, 127, 128):
+        assert L.mstf_value_record_bytes(k, 16) == L.mstf_value_record_bytes(k, 0) == 2 * O.k_pad_of(k)
+        assert L.mstf_value_record_bytes(k, 4) == O.q4_record_bytes(k)
+    assert L.mstf_value_record_bytes(39, 8) == -1
+    sizes = M.buffer_bytes(cfg(value_bits=4))
+    assert sizes[M.BUFFERS.index("values_k")] == 4 * 100 * 32 + 16
+    assert sizes[M.BUFFERS.index("values_v")] == 4 * 100 * 48 + 16
+    assert L.mstf_cache_buffer_bytes(ctypes.byref(cfg(value_bits=5)), (ctypes.c_size_t * M.NUM_BUFFERS)()) == -1
+
+
 def cfg(**kw):
     base = dict(batch=2, num_q_heads=8, num_kv_heads=2, head_dim=128, keep_k=39, keep_v=64, window=32,
-                capacity=100)
+                capacity=100, value_bits=16)
     base.update(kw)
     return M.Config(*[base[n] for n, _ in M.Config._fields_])
 
