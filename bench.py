@@ -46,6 +46,12 @@ WORKLOADS = {
                sk=0.7, sv=0.7),
     "C5": dict(desc="Llama-3-8B shape, 16K context, batch 64 per GPU, 70% sparsity", batch=64, hq=32, hkv=8,
                T=16384, sk=0.7, sv=0.7),
+    # NEXT-4: the C4 shape with the prune-then-quantize payload (4-bit codes + fp16 scale / zero per
+    # token, tab:joint_quant)
+    "C4_q4": dict(desc="Llama-3-8B shape, 128K context, batch 8, 70% sparsity, 4-bit payload (NEXT-4)", batch=8,
+                  hq=32, hkv=8, T=131072, sk=0.7, sv=0.7, vbits=4),
+    "C2_q4": dict(desc="Llama-3-8B shape decode, 4K context, batch 16, 70% sparsity, 4-bit payload (NEXT-4)",
+                  batch=16, hq=32, hkv=8, T=4096, sk=0.7, sv=0.7, vbits=4),
 }
 DEFAULT_WORKLOAD = "C4"   # the largest single-GPU configuration of BASELINE.json (128K context)
 SPEC_HBM_GBS = 8000.0     # nominal B200 HBM3e (DGX figure; B200_PROFILING.md: 7.7 HGX / 8 DGX)
@@ -60,7 +66,8 @@ def config_of(args, cfg, world, L, extra=None):
     B = cfg["batch"]
     c = {"workload": args.workload, "desc": cfg["desc"], "batch_per_gpu": B, "global_batch": B * world,
          "num_q_heads": cfg["hq"], "num_kv_heads": cfg["hkv"], "head_dim": 128, "context": cfg["T"],
-         "keep_k": keep_of(cfg["sk"]), "keep_v": keep_of(cfg["sv"]), "window": W_WINDOW, "layers": L}
+         "keep_k": keep_of(cfg["sk"]), "keep_v": keep_of(cfg["sv"]), "window": W_WINDOW, "layers": L,
+         "value_bits": cfg.get("vbits", 16)}
     if extra:
         c.update(extra)
     return c
@@ -84,14 +91,19 @@ def kpad_of(k):
     return (k + 7) // 8 * 8
 
 
-def algorithmic_bytes(U, G, n_comp, n_win, keep_k, keep_v, d=128, out_bytes=2, append=False):
+def record_bytes(k, vbits=16):
+    """Bytes of one token's value record: 2 k_pad (fp16) or the 4-bit record (R26)."""
+    return 2 * kpad_of(k) if vbits == 16 else (4 + (k + 1) // 2 + 15) // 16 * 16
+
+
+def algorithmic_bytes(U, G, n_comp, n_win, keep_k, keep_v, d=128, out_bytes=2, append=False, vbits=16):
     """Bytes one sparse attention call must move: compressed K and V records
     (bitmaps d/8 B + packed values 2*kpad B each; offsets are not read), the dense window,
     q and the output. Split partials are an implementation artefact and are not counted.
     append=True adds one decode step's append (a4): the new K and V tokens read, the evicted
     window tokens read and written back compressed (record + u32 offsets), the new tokens
     written into the ring."""
-    rec = (d // 8 + 2 * kpad_of(keep_k)) + (d // 8 + 2 * kpad_of(keep_v))
+    rec = (d // 8 + record_bytes(keep_k, vbits)) + (d // 8 + record_bytes(keep_v, vbits))
     b = U * (n_comp * rec + n_win * 4 * d + G * d * 2 + G * d * out_bytes)
     if append:
         b += U * (2 * 2 * d + 2 * 2 * d + rec + 2 * 8 + 2 * 2 * d)
@@ -235,7 +247,7 @@ def oracle_sample(cfg, seconds=10.0, max_units=64):
         for u in range(min(U, max_units)):
             K = synth.fp16_np_rows((U, T, d), synth.seed_for(2, 0), u * T, T).view(np.uint16)
             V = synth.fp16_np_rows((U, T, d), synth.seed_for(2, 1), u * T, T).view(np.uint16)
-            oc = O.OracleCache(1, d, kk, kv, W_WINDOW, T + 1)
+            oc = O.OracleCache(1, d, kk, kv, W_WINDOW, T + 1, value_bits=cfg.get("vbits", 16))
             oc.prefill(K[None, :T - 1], V[None, :T - 1])
             q = synth.fp16_np_rows((U, G, d), synth.seed_for(2, 2), u * G, G).view(np.uint16)
             t0 = time.perf_counter()
@@ -367,6 +379,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     B, hq, hkv, T = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["T"]
     U, G, d = B * hkv, hq // hkv, 128
     kk, kv = keep_of(cfg["sk"]), keep_of(cfg["sv"])
+    vbits = cfg.get("vbits", 16)
     L = LAYERS if args.layers is None else args.layers
     K_steps, W_steps = args.steps, args.warmup
     # warm-up, the headline timed pass (no events between a step's kernels, so programmatic
@@ -389,7 +402,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         seed = synth.seed_for(2, 10 * l + 1000 * rank)
         Kl = synth.fp16_torch((U, T + total_steps, d), seed, device=dev)
         Vl = synth.fp16_torch((U, T + total_steps, d), seed + 1, device=dev)
-        c = M.MustafarCache(B, hq, hkv, d, kk, kv, W_WINDOW, cap, device=dev)
+        c = M.MustafarCache(B, hq, hkv, d, kk, kv, W_WINDOW, cap, device=dev, value_bits=vbits)
         Kp, Vp = Kl[:, :T0].contiguous(), Vl[:, :T0].contiguous()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -408,7 +421,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     pf_us = pf_us[len(pf_us) // 2]
     kpk, kpv = kpad_of(kk), kpad_of(kv)
     nc0, nw0 = max(T0 - W_WINDOW, 0), min(T0, W_WINDOW)
-    pf_bytes = U * (2 * T0 * d * 2 + nc0 * (2 * (d // 8 + 4 * (d // 64)) + 2 * kpk + 2 * kpv) + 2 * nw0 * d * 2)
+    pf_bytes = U * (2 * T0 * d * 2 + nc0 * (2 * (d // 8 + 4 * (d // 64)) + record_bytes(kk, vbits) +
+                                             record_bytes(kv, vbits)) + 2 * nw0 * d * 2)
     # per-step decode inputs: q [U,G,d], k_new/v_new [U,d] for every (step, layer), one slab per step
     per_layer = U * G * d + 2 * U * d
     gen = synth.fp16_torch((total_steps, L, per_layer), synth.seed_for(2, 7 + rank), device=dev)
@@ -602,7 +616,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms, attn_us, e2e_ms = vals.tolist()[:3]
 
-    bytes_attn = algorithmic_bytes(U, G, n_comp, n_win, kk, kv, append=True)
+    bytes_attn = algorithmic_bytes(U, G, n_comp, n_win, kk, kv, append=True, vbits=vbits)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -630,7 +644,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f16 (fp32 accumulate)",
+        "dtype": "f16 (fp32 accumulate)" if vbits == 16 else "u4 codes + f16 scale/zero (fp16 MMA, fp32 accumulate)",
         "data": "synthetic (seeded splitmix64 -> fp16 ~N(0,1)); no model weights",
         "config": config_of(args, cfg, world, L, {
             "parallelism": par,

@@ -31,8 +31,9 @@ def compare_unit(bufs, u, oc, note):
     window ring and both counters, bit-exact against the oracle's one-unit cache."""
     nc, nw = int(oc.n_comp[0]), int(oc.n_win[0])
     assert int(bufs["n_comp"][u]) == nc and int(bufs["n_win"][u]) == nw, note
-    for name, dt in (("bitmap_k", np.uint64), ("bitmap_v", np.uint64), ("values_k", np.uint16),
-                     ("values_v", np.uint16), ("offsets_k", np.uint32), ("offsets_v", np.uint32)):
+    vdt = oc.values_k.dtype   # uint16 fp16 values, or uint8 4-bit records (NEXT-4)
+    for name, dt in (("bitmap_k", np.uint64), ("bitmap_v", np.uint64), ("values_k", vdt),
+                     ("values_v", vdt), ("offsets_k", np.uint32), ("offsets_v", np.uint32)):
         g = bufs[name][u, :nc].cpu().numpy().view(dt)
         assert np.array_equal(g, getattr(oc, name)[0, :nc]), (note, name)
     if oc.W:
@@ -49,10 +50,15 @@ CASES = {
     "C3_mha_32k": (1, 32, 32, 32768, 0.7, 0.7, (0, 31)),
     "C4_128k_b8": (8, 32, 8, 131072, 0.7, 0.7, (5, 63)),
     "C5_16k_b64": (64, 32, 8, 16384, 0.7, 0.7, (0, 300, 511)),
+    "C4_128k_b8_q4": (8, 32, 8, 131072, 0.7, 0.7, (5, 63)),   # 4-bit payload (NEXT-4)
 }
 
 
-@pytest.mark.parametrize("name", list(CASES))
+def vbits_of(name):
+    return 4 if name.endswith("_q4") else 16
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if not n.endswith("_q4")])
 def test_fullsize_sampled(M, name):
     B, hq, hkv, T, sk, sv, sample = CASES[name]
     U, G, d, W = B * hkv, hq // hkv, 128, 32
@@ -80,7 +86,7 @@ def test_fullsize_sampled(M, name):
         assert err <= TOL, (name, u, err)
 
 
-@pytest.mark.parametrize("name", ["C2_b16_s70", "C3_mha_32k", "C4_128k_b8", "C5_16k_b64"])
+@pytest.mark.parametrize("name", ["C2_b16_s70", "C3_mha_32k", "C4_128k_b8", "C5_16k_b64", "C4_128k_b8_q4"])
 def test_fullsize_decode_step_sampled(M, name):
     """One fused decode step (mstf_decode_step: the append inside the attention launch) at full
     size -- the launch configuration bench.py times -- against the oracle on sampled units:
@@ -92,7 +98,7 @@ def test_fullsize_decode_step_sampled(M, name):
     K = synth.fp16_torch((U, T + 1, d), sK, device="cuda")
     V = synth.fp16_torch((U, T + 1, d), sV, device="cuda")
     q = synth.fp16_torch((U, G, d), sQ, device="cuda")
-    gc = M.MustafarCache(B, hq, hkv, d, kk, kv, W, T + 1)
+    gc = M.MustafarCache(B, hq, hkv, d, kk, kv, W, T + 1, value_bits=vbits_of(name))
     gc.prune_compress_kv(K[:, :T].contiguous(), V[:, :T].contiguous())
     kn, vn = K[:, T].contiguous(), V[:, T].contiguous()
     del K, V
@@ -104,7 +110,7 @@ def test_fullsize_decode_step_sampled(M, name):
     for u in sample:
         Ku = synth.fp16_np_rows((U, T + 1, d), sK, u * (T + 1), T + 1).view(np.uint16)
         Vu = synth.fp16_np_rows((U, T + 1, d), sV, u * (T + 1), T + 1).view(np.uint16)
-        oc = O.OracleCache(1, d, kk, kv, W, T + 1)
+        oc = O.OracleCache(1, d, kk, kv, W, T + 1, value_bits=vbits_of(name))
         oc.prefill(Ku[None, :T], Vu[None, :T])
         oc.append(Ku[None, T], Vu[None, T])
         compare_unit(bufs, u, oc, f"{name} step u={u}")
