@@ -233,36 +233,51 @@ __device__ __forceinline__ uint32_t hfma2_u(uint32_t a, uint32_t b, uint32_t c) 
   __half2 r = __hfma2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b), *reinterpret_cast<__half2*>(&c));
   return *reinterpret_cast<uint32_t*>(&r);
 }
+// One pair of codes (bytes i of the low / high nibble words) -> f16(c * scale + zero) x 2.
+__device__ __forceinline__ uint32_t dequant_pair(uint32_t lo, uint32_t hi, int i, uint32_t sc2, uint32_t z2) {
+  const uint32_t t = (prmt(lo, hi, (uint32_t)(((4 + i) << 8) | i)) & 0x00FF00FFu) | 0x64006400u;
+  return hfma2_u(hsub2_u(t, 0x64006400u), sc2, z2);
+}
+// Eight values (code word w) -> pair entries Y[8c .. 8c+7] at d; prev = last raw pair word.
+__device__ __forceinline__ void q4_word_pairs(uint32_t w, uint32_t sc2, uint32_t z2, uint32_t d, uint32_t& prev) {
+  const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
+  uint32_t R[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) R[i] = dequant_pair(lo, hi, i, sc2, z2);
+  sts32(d, prmt(prev, R[0], 0x5432));
+  sts32(d + 4, R[0]);
+  sts32(d + 8, prmt(R[0], R[1], 0x5432));
+  sts32(d + 12, R[1]);
+  sts32(d + 16, prmt(R[1], R[2], 0x5432));
+  sts32(d + 20, R[2]);
+  sts32(d + 24, prmt(R[2], R[3], 0x5432));
+  sts32(d + 28, R[3]);
+  prev = R[3];
+}
 template <int NCH>
 __device__ __forceinline__ void build_token_q4(uint32_t rec, uint32_t ydst, int nch_rt) {
-  const int nch = NCH ? NCH : nch_rt;
-  const uint32_t sz = lds32(rec);
-  const uint32_t sc2 = prmt(sz, 0u, 0x1010), z2 = prmt(sz, 0u, 0x3232);
   uint32_t prev = 0;
   sts32(ydst, 0u);
+  if constexpr (NCH > 0) {
+    // the whole record in 16-byte loads (records are 16-byte aligned; scalar loads of 32-byte
+    // strided records would hit every bank group 4 times)
+    constexpr int RQ = (4 * NCH + 4 + 15) / 16 * 16;
+    uint32_t wv[RQ / 4];
 #pragma unroll
-  for (int c = 0; c < (NCH ? NCH : 16); ++c) {
-    if (!NCH && c >= nch) break;
-    const uint32_t w = lds32(rec + 4 + 4 * c);
-    const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;
-    uint32_t R[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t t = (prmt(lo, hi, (uint32_t)(((4 + i) << 8) | i)) & 0x00FF00FFu) | 0x64006400u;
-      R[i] = hfma2_u(hsub2_u(t, 0x64006400u), sc2, z2);
+    for (int i = 0; i < RQ / 16; ++i) {
+      const uint4 a = lds128(rec + 16 * i);
+      wv[4 * i] = a.x; wv[4 * i + 1] = a.y; wv[4 * i + 2] = a.z; wv[4 * i + 3] = a.w;
     }
-    const uint32_t d = ydst + 32u * c;
-    sts32(d, prmt(prev, R[0], 0x5432));
-    sts32(d + 4, R[0]);
-    sts32(d + 8, prmt(R[0], R[1], 0x5432));
-    sts32(d + 12, R[1]);
-    sts32(d + 16, prmt(R[1], R[2], 0x5432));
-    sts32(d + 20, R[2]);
-    sts32(d + 24, prmt(R[2], R[3], 0x5432));
-    sts32(d + 28, R[3]);
-    prev = R[3];
+    const uint32_t sc2 = prmt(wv[0], 0u, 0x1010), z2 = prmt(wv[0], 0u, 0x3232);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) q4_word_pairs(wv[1 + c], sc2, z2, ydst + 32u * c, prev);
+    sts32(ydst + 32u * NCH, prmt(prev, 0u, 0x5432));
+  } else {
+    const uint32_t sz = lds32(rec);
+    const uint32_t sc2 = prmt(sz, 0u, 0x1010), z2 = prmt(sz, 0u, 0x3232);
+    for (int c = 0; c < nch_rt; ++c) q4_word_pairs(lds32(rec + 4 + 4 * c), sc2, z2, ydst + 32u * c, prev);
+    sts32(ydst + 32u * nch_rt, prmt(prev, 0u, 0x5432));
   }
-  sts32(ydst + 32u * nch, prmt(prev, 0u, 0x5432));
 }
 
 // ---------------------------------------------------------------- schedule (device side)
@@ -1006,8 +1021,11 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   const bool g8 = G > 4;
   void* kern = nullptr;
   const int nk = c.kpad[0] / 8, nv = c.kpad[1] / 8;
-  if (c.vbits == 4) kern = pick_kernel<0, 0, true>(g8);
-  else if (nk == nv && nk == 5) kern = pick_kernel<5, 5>(g8);
+  if (c.vbits == 4) {
+    if (nk == nv && nk == 5) kern = pick_kernel<5, 5, true>(g8);
+    else if (nk == nv && nk == 8) kern = pick_kernel<8, 8, true>(g8);
+    else kern = pick_kernel<0, 0, true>(g8);
+  } else if (nk == nv && nk == 5) kern = pick_kernel<5, 5>(g8);
   else if (nk == nv && nk == 8) kern = pick_kernel<8, 8>(g8);
   else if (nk == nv && nk == 4) kern = pick_kernel<4, 4>(g8);
   else if (nk == nv && nk == 2) kern = pick_kernel<2, 2>(g8);
