@@ -45,6 +45,9 @@ namespace mstf {
 
 namespace {
 
+#ifndef MSTF_B128
+#define MSTF_B128 1  // pair arrays written with 16-byte stores (dev A/B: 0 = 4-byte stores)
+#endif
 constexpr int kWNst = 2;          // TMA ring depth per warp (blocks in flight)
 constexpr int kWMaxWarps = 16;    // warps per CTA (one CTA per SM, <= 128 registers per thread)
 constexpr int kWHdrInts = 16;     // workspace header: [0] S (total cost), [1] cost per unit (0: ragged)
@@ -88,6 +91,8 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
   return d;
 }
+// Opaque copy: keeps a precomputed address in a register of its own (the compiler would otherwise
+// re-associate base + 4 (e + popc) and spend an add per gather).
 __device__ __forceinline__ uint32_t opaque(uint32_t x) {
   asm("mov.b32 %0, %0;" : "+r"(x));
   return x;
@@ -102,24 +107,11 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-// Gather only when the dibit keeps a channel (mask != 0): idle lanes take no bank slot. The
-// loaded word replaces the address in the same register; a skipped load leaves the address
-// there, which the AND with the (zero) mask clears -- no zeroed register per gather.
-// MSTF_GATHER_PRED=0 (dev A/B): every lane loads (one instruction less, more bank conflicts).
-#ifndef MSTF_GATHER_PRED
-#define MSTF_GATHER_PRED 1
-#endif
-__device__ __forceinline__ uint32_t lds_masked(uint32_t a, uint32_t mask) {
-#if MSTF_GATHER_PRED
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p ld.shared.u32 %0, [%0];\n\t}"
-               : "+r"(a) : "r"(mask) : "memory");
-#else
-  asm volatile("ld.shared.u32 %0, [%0];" : "+r"(a) : : "memory");
-#endif
-  return a & mask;
 }
 __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -151,62 +143,74 @@ __device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
 
-// Mask for dibit J of a word (channels 2J, 2J+1 -> halves lo, hi): 0xFFFF where kept.
-// cp[s] = w << (7 - s) puts bit 8m+s at the sign bit of byte m; prmt's sign-replicate mode
-// turns the two needed sign bits into byte masks.
-template <int J>
-__device__ __forceinline__ uint32_t dibit_mask(const uint32_t (&cp)[8]) {
-  constexpr int m = J / 4, s0 = 2 * (J % 4);
-  constexpr uint32_t lo = 8 | m, hi = 8 | (4 + m);
-  constexpr uint32_t sel = lo | (lo << 4) | (hi << 8) | (hi << 12);
-  return prmt(cp[s0], cp[s0 + 1], sel);
+// Byte-mask of one channel pair: x has the pair's low bit at the sign bit of byte M, y its high
+// bit; prmt's sign-replicate mode turns them into 0xFFFF halves (kept) or 0x0000 (pruned).
+template <int M>
+__device__ __forceinline__ uint32_t pair_mask(uint32_t x, uint32_t y) {
+  constexpr uint32_t lo = 8 | M, hi = 8 | (4 + M);
+  return prmt(x, y, lo | (lo << 4) | (hi << 8) | (hi << 12));
+}
+// One gather: pair entry Y[idx] of a token's pair array (base = its entry e_q, scaled) ANDed with
+// the pair's mask. Every lane loads (no predicate): in the consecutive-pair mapping below the
+// lanes of one token read a few neighbouring words, so a pruned pair's lane adds no bank slot.
+__device__ __forceinline__ uint32_t gather1(uint32_t base, uint32_t cnt, uint32_t mask) {
+  return lds32(base + 4u * cnt) & mask;
 }
 
-// Expand the 16 dibits of word w: out[j] = channel pair (2j, 2j+1), zeros where pruned.
-// base = shared address of pair entry e (e = kept channels of the token before this word).
-__device__ __forceinline__ void gather16(uint32_t w, uint32_t base_in, uint32_t (&out)[16]) {
-  const uint32_t base = opaque(base_in);
-  uint32_t cp[8];
+// Per-token, per-word state of the consecutive-pair gathers:
+//   x[q] = w_q << sx, y[q] = w_q << (sx - 1): the lane's pair bits at byte sign positions;
+//   B[q] = address of pair entry e_q (kept channels of the token before word q).
+// The kept count up to and including a pair's low channel is e_q + popc(x[q] << k) for an
+// immediate k that drops the bits above it, so Y[e_q + that] is the pair (R8, R6).
+struct TokGather {
+  uint32_t x[4], y[4], B[4];
+};
+__device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t base, uint32_t sx) {
+  const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+  uint32_t b = base;
 #pragma unroll
-  for (int s = 0; s < 8; ++s) cp[s] = w * (1u << (7 - s));
-#define MSTF_G(J) out[J] = lds_masked(base + 4u * __popc(w * (1u << (31 - 2 * J))), dibit_mask<J>(cp));
-  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
-  MSTF_G(8) MSTF_G(9) MSTF_G(10) MSTF_G(11) MSTF_G(12) MSTF_G(13) MSTF_G(14) MSTF_G(15)
-#undef MSTF_G
+  for (int q = 0; q < 4; ++q) {
+    tg.x[q] = ww[q] << sx;
+    tg.y[q] = ww[q] << (sx - 1);
+    tg.B[q] = opaque(b);
+    b += 4u * __popc(ww[q]);
+  }
 }
-// Expand 8 dibits of two half-words at once: hw2 = (half-word of token b) << 16 | (half-word
-// of token a); bases of the two tokens' pair entries. outa/outb[j] = channel pair j.
-__device__ __forceinline__ void gather8x2(uint32_t hw2, uint32_t base_a_in, uint32_t base_b_in, uint32_t (&outa)[8],
-                                          uint32_t (&outb)[8]) {
-  const uint32_t base_a = opaque(base_a_in), base_b = opaque(base_b_in);
-  uint32_t cp[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) cp[s] = hw2 * (1u << (7 - s));
-  const uint32_t hb = hw2 >> 16;
-// hw2 << (31 - 2J) keeps exactly the low half-word's bits <= 2J (2J <= 14).
-#define MSTF_G(J)                                                                    \
-  outa[J] = lds_masked(base_a + 4u * __popc(hw2 * (1u << (31 - 2 * J))), dibit_mask<J>(cp)); \
-  outb[J] = lds_masked(base_b + 4u * __popc(hb * (1u << (31 - 2 * J))), dibit_mask<8 + J>(cp));
-  MSTF_G(0) MSTF_G(1) MSTF_G(2) MSTF_G(3) MSTF_G(4) MSTF_G(5) MSTF_G(6) MSTF_G(7)
-#undef MSTF_G
+// K (score A operand): gather slot j = 2s + hh of lane t is pair 8s + 4hh + t, i.e. channels
+// 16s + 8hh + 2t, +1 -- the natural m16n8k16 k order. Word q = j >> 2, byte m = j & 3; the
+// lane's bit in byte m is bit 8m + 2t, at bit 8m + 7 of x (sx = 7 - 2t).
+template <int J>
+__device__ __forceinline__ uint32_t gather_k(const TokGather& tg) {
+  constexpr int q = J >> 2, m = J & 3;
+  const uint32_t cnt = __popc(m == 3 ? tg.x[q] : tg.x[q] << (24 - 8 * m));
+  return gather1(tg.B[q], cnt, pair_mask<m>(tg.x[q], tg.y[q]));
+}
+// V (value A operand): row r (0: g, 1: g + 8) of m-tile mt is pair 16mt + 8r + g, i.e. word mt,
+// bit 16r + 2g, at bit 16r + 15 of x (sx = 15 - 2g): byte 1 + 2r.
+template <int MT, int R>
+__device__ __forceinline__ uint32_t gather_v(const TokGather& tg) {
+  const uint32_t cnt = __popc(R ? tg.x[MT] : tg.x[MT] << 16);
+  return gather1(tg.B[MT], cnt, pair_mask<1 + 2 * R>(tg.x[MT], tg.y[MT]));
 }
 
 // Shifted pair arrays of the 16 tokens of both tensors in a stage, one token per lane (lanes
 // 0-15: K tokens 0-15, lanes 16-31: V tokens 0-15): Y[m] = (h[m-1], h[m]), m = 0..kp
 // (h[-1] = h[kp] = 0) at ydst + 4 * (tau * sw + m). Odd entries are the raw words, even ones
-// one prmt each; scalar stores (no register shuffling into 16-byte groups). With sw = kp + 2
-// (2 mod 4) and the V region 1 word past a 32-word boundary, the 32 lanes of every store hit 32
-// distinct banks. raw = this lane's token record in the stage.
+// one prmt each; four entries per 16-byte store. With sw = kp + 4 (4 mod 8 words) the 8 lanes of
+// every quarter-warp store phase hit 8 distinct 16-byte bank groups. raw = this lane's record.
 template <int NCH>
 __device__ __forceinline__ void build_token(uint32_t raw, uint32_t ydst, int nch_rt) {
   const int nch = NCH ? NCH : nch_rt;
   uint32_t prev = 0;
-  sts32(ydst, 0u);  // Y[0].lo = h[-1] = 0 (hi = h[0], rewritten below)
 #pragma unroll
   for (int c = 0; c < (NCH ? NCH : 16); ++c) {
     if (!NCH && c >= nch) break;
     const uint4 a = lds128(raw + 16 * c);
     const uint32_t d = ydst + 32u * c;
+#if MSTF_B128
+    sts128(d, prmt(prev, a.x, 0x5432), a.x, prmt(a.x, a.y, 0x5432), a.y);
+    sts128(d + 16, prmt(a.y, a.z, 0x5432), a.z, prmt(a.z, a.w, 0x5432), a.w);
+#else
     sts32(d, prmt(prev, a.x, 0x5432));
     sts32(d + 4, a.x);
     sts32(d + 8, prmt(a.x, a.y, 0x5432));
@@ -215,6 +219,7 @@ __device__ __forceinline__ void build_token(uint32_t raw, uint32_t ydst, int nch
     sts32(d + 20, a.z);
     sts32(d + 24, prmt(a.z, a.w, 0x5432));
     sts32(d + 28, a.w);
+#endif
     prev = a.w;
   }
   sts32(ydst + 32u * nch, prmt(prev, 0u, 0x5432));
@@ -244,6 +249,10 @@ __device__ __forceinline__ void q4_word_pairs(uint32_t w, uint32_t sc2, uint32_t
   uint32_t R[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) R[i] = dequant_pair(lo, hi, i, sc2, z2);
+#if MSTF_B128
+  sts128(d, prmt(prev, R[0], 0x5432), R[0], prmt(R[0], R[1], 0x5432), R[1]);
+  sts128(d + 16, prmt(R[1], R[2], 0x5432), R[2], prmt(R[2], R[3], 0x5432), R[3]);
+#else
   sts32(d, prmt(prev, R[0], 0x5432));
   sts32(d + 4, R[0]);
   sts32(d + 8, prmt(R[0], R[1], 0x5432));
@@ -252,12 +261,12 @@ __device__ __forceinline__ void q4_word_pairs(uint32_t w, uint32_t sc2, uint32_t
   sts32(d + 20, R[2]);
   sts32(d + 24, prmt(R[2], R[3], 0x5432));
   sts32(d + 28, R[3]);
+#endif
   prev = R[3];
 }
 template <int NCH>
 __device__ __forceinline__ void build_token_q4(uint32_t rec, uint32_t ydst, int nch_rt) {
   uint32_t prev = 0;
-  sts32(ydst, 0u);
   if constexpr (NCH > 0) {
     // the whole record in 16-byte loads (records are 16-byte aligned; scalar loads of 32-byte
     // strided records would hit every bank group 4 times)
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   // per-warp region: [stages kWNst x stage_bytes][pairs K 16 x swk words][pairs V][mbarriers]
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(warp * p.warp_bytes);
   const uint32_t ypk = wbase + (uint32_t)(kWNst * p.stage_bytes);  // 128-byte aligned
-  const uint32_t ypv = ypk + ((64u * (uint32_t)p.swk + 127u) & ~127u) + 4u;
+  const uint32_t ypv = ypk + ((64u * (uint32_t)p.swk + 127u) & ~127u) + (MSTF_B128 ? 0u : 4u);
   const uint32_t bar0 = (ypv + 64u * (uint32_t)p.swv + 7u) & ~7u;
   if (lane == 0) {
 #pragma unroll
@@ -490,38 +499,47 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   auto softmax = [&](const float (&sc)[4], bool vg, bool vg8, uint32_t (&bb)[NT][4]) {
     const float x0 = vg ? sc[0] * p.scale_log2 : -INFINITY, x1 = vg ? sc[1] * p.scale_log2 : -INFINITY;
     const float x2 = vg8 ? sc[2] * p.scale_log2 : -INFINITY, x3 = vg8 ? sc[3] * p.scale_log2 : -INFINITY;
-    float b0 = fmaxf(x0, x2), b1 = fmaxf(x1, x3);
+    // Lazy rescale: the running reference max m moves only when a score exceeds it by more than
+    // kLazyLog2 (then P <= 2^kLazyLog2 in fp16, exact to its 11 bits; l and o are fp32, and the
+    // combine merges slots by their own m, so any reference value is exact algebra). The common
+    // case skips the max reduction and the accumulator rescale.
+    constexpr float kLazyLog2 = 8.f;
+    const bool need = fmaxf(fmaxf(x0, x2) - m0, fmaxf(x1, x3) - m1) > kLazyLog2;
+    if (__any_sync(0xffffffffu, need)) {
+      float b0 = fmaxf(x0, x2), b1 = fmaxf(x1, x3);
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      b0 = fmaxf(b0, __shfl_xor_sync(0xffffffffu, b0, o));
-      b1 = fmaxf(b1, __shfl_xor_sync(0xffffffffu, b1, o));
-    }
-    const float n0 = fmaxf(m0, b0), n1 = fmaxf(m1, b1);
-    const float a0 = ex2(m0 - n0), a1 = ex2(m1 - n1);
-    const float p0 = ex2(x0 - n0), p1 = ex2(x1 - n1), p2 = ex2(x2 - n0), p3 = ex2(x3 - n1);
-    l0 = l0 * a0 + (p0 + p2);
-    l1 = l1 * a1 + (p1 + p3);
-    m0 = n0;
-    m1 = n1;
-    // accumulator columns 2t, 2t+1 of tile nt hold heads (2t & 3) + 4 nt, (2t+1 & 3) + 4 nt
-    float aa[NT][2];
-    if constexpr (G8) {
-      const float o0 = __shfl_xor_sync(0xffffffffu, a0, 2), o1 = __shfl_xor_sync(0xffffffffu, a1, 2);
-      aa[0][0] = t < 2 ? a0 : o0; aa[0][1] = t < 2 ? a1 : o1;
-      aa[1][0] = t < 2 ? o0 : a0; aa[1][1] = t < 2 ? o1 : a1;
-    } else {
-      aa[0][0] = a0;
-      aa[0][1] = a1;
-    }
+      for (int o = 4; o < 32; o <<= 1) {
+        b0 = fmaxf(b0, __shfl_xor_sync(0xffffffffu, b0, o));
+        b1 = fmaxf(b1, __shfl_xor_sync(0xffffffffu, b1, o));
+      }
+      const float n0 = fmaxf(m0, b0), n1 = fmaxf(m1, b1);
+      const float a0 = ex2(m0 - n0), a1 = ex2(m1 - n1);
+      l0 *= a0;
+      l1 *= a1;
+      m0 = n0;
+      m1 = n1;
+      // accumulator columns 2t, 2t+1 of tile nt hold heads (2t & 3) + 4 nt, (2t+1 & 3) + 4 nt
+      float aa[NT][2];
+      if constexpr (G8) {
+        const float o0 = __shfl_xor_sync(0xffffffffu, a0, 2), o1 = __shfl_xor_sync(0xffffffffu, a1, 2);
+        aa[0][0] = t < 2 ? a0 : o0; aa[0][1] = t < 2 ? a1 : o1;
+        aa[1][0] = t < 2 ? o0 : a0; aa[1][1] = t < 2 ? o1 : a1;
+      } else {
+        aa[0][0] = a0;
+        aa[0][1] = a1;
+      }
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      // unconditional (FMA pipe, branch-free: loads of the next phase can be scheduled across)
+      for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[nt][i][0] *= aa[nt][0]; acc[nt][i][1] *= aa[nt][1];
-        acc[nt][i][2] *= aa[nt][0]; acc[nt][i][3] *= aa[nt][1];
+        for (int i = 0; i < 4; ++i) {
+          acc[nt][i][0] *= aa[nt][0]; acc[nt][i][1] *= aa[nt][1];
+          acc[nt][i][2] *= aa[nt][0]; acc[nt][i][3] *= aa[nt][1];
+        }
       }
     }
+    const float p0 = ex2(x0 - m0), p1 = ex2(x1 - m1), p2 = ex2(x2 - m0), p3 = ex2(x3 - m1);
+    l0 += p0 + p2;
+    l1 += p1 + p3;
     // P^T tiles (tokens g / g+8, heads 2t, 2t+1) -> P tiles [head g][tokens 2t, 2t+1 (+8)]
     uint32_t M[2] = {movmatrix_t(pack_half2(p0, p1)), movmatrix_t(pack_half2(p2, p3))};
 #pragma unroll
@@ -559,16 +577,13 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       if (lane < p.G) *reinterpret_cast<float2*>(p.ws_ml + (((size_t)P + u) * p.G + lane) * 2) = make_float2(-INFINITY, 0.f);
       continue;
     }
-    if (u != qu) {  // q of the unit: head column g (g & 3 when G <= 4), channels 32t..32t+31
-      qu = u;
+    if (u != qu) {  // q of the unit: head column g (g & 3 when G <= 4); k-step s: channels
+      qu = u;        // 16s + 2t, +1 (qf[2s]) and 16s + 8 + 2t, +1 (qf[2s+1]) -- word 4j + t of slot j
       const int h = G8 ? g : (g & 3);
       if (h < p.G) {
-        const uint4* qp = reinterpret_cast<const uint4*>(p.q + ((size_t)u * p.G + h) * kD + 32 * t);
+        const uint32_t* qp = reinterpret_cast<const uint32_t*>(p.q + ((size_t)u * p.G + h) * kD) + t;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint4 x = __ldg(qp + i);
-          qf[4 * i] = x.x; qf[4 * i + 1] = x.y; qf[4 * i + 2] = x.z; qf[4 * i + 3] = x.w;
-        }
+        for (int i = 0; i < 16; ++i) qf[i] = __ldg(qp + 4 * i);
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) qf[i] = 0u;
@@ -596,14 +611,14 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
         build_token_q4<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
       else
         build_token<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
-      // K bitmap word t of tokens g, g + 8; V half-word g of tokens 2t, 2t+1, 8+2t, 9+2t
-      const uint32_t kw0 = g < nvalid ? lds32(st + 16 * g + 4 * t) : 0u;
-      const uint32_t kw1 = g + 8 < nvalid ? lds32(st + 16 * (g + 8) + 4 * t) : 0u;
+      // bitmaps (4 words) of K tokens g, g + 8 and V tokens 2t, 2t+1, 8+2t, 9+2t (R5, R6)
+      const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+      const uint4 kb0 = g < nvalid ? lds128(st + 16 * g) : z4;
+      const uint4 kb1 = g + 8 < nvalid ? lds128(st + 16 * (g + 8)) : z4;
       const int tk[4] = {2 * t, 2 * t + 1, 8 + 2 * t, 9 + 2 * t};
-      uint32_t hw[4];
+      uint4 vbm[4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
-        hw[x] = tk[x] < nvalid ? (lds32(st + p.off_vbm + 16 * tk[x] + 4 * (g >> 1)) >> (16 * (g & 1))) & 0xFFFFu : 0u;
+      for (int x = 0; x < 4; ++x) vbm[x] = tk[x] < nvalid ? lds128(st + p.off_vbm + 16 * tk[x]) : z4;
       __syncwarp();
       // the stage is fully read: refill it with block cseq + kWNst (WAR vs the TMA write)
       if (!pdone) {
@@ -614,43 +629,43 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
         ++pseq;
         p_advance();
       }
-      // exclusive prefixes: K over the 4 words of a token (lanes t), V over the 8 half-words
-      // (lanes g, stride 4), 4 tokens in 4 bytes
-      const uint32_t pk = __popc(kw0) | (__popc(kw1) << 16);
-      uint32_t ik = pk;
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, ik, o, 4);
-        if (t >= o) ik += y;
-      }
-      const uint32_t ek = ik - pk;
-      const uint32_t pv = __popc(hw[0]) | (__popc(hw[1]) << 8) | (__popc(hw[2]) << 16) | (__popc(hw[3]) << 24);
-      uint32_t iv = pv;
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, iv, 4 * o);
-        if (g >= o) iv += y;
-      }
-      const uint32_t ev = iv - pv;
       uint32_t bb[NT][4];
+      // a5: S^T += K_blk . q^T, k-step by k-step (two accumulation chains)
+      float sc[4];
+      {
+        TokGather t0, t1;
+        tok_prep(t0, kb0, ypk + 4u * (uint32_t)(g * p.swk), 7u - 2u * (uint32_t)t);
+        tok_prep(t1, kb1, ypk + 4u * (uint32_t)((g + 8) * p.swk), 7u - 2u * (uint32_t)t);
+        float s2[4] = {0.f, 0.f, 0.f, 0.f};
+        sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
+#define MSTF_KS(S)                                                                                              \
+  mma16816((S & 1) ? s2 : sc, gather_k<2 * S>(t0), gather_k<2 * S>(t1), gather_k<2 * S + 1>(t0), gather_k<2 * S + 1>(t1), \
+           qf[2 * S], qf[2 * S + 1]);
+        MSTF_KS(0) MSTF_KS(1) MSTF_KS(2) MSTF_KS(3) MSTF_KS(4) MSTF_KS(5) MSTF_KS(6) MSTF_KS(7)
+#undef MSTF_KS
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sc[i] += s2[i];
+      }
+      // a8, k-step ks: tokens tk[2ks] (va) and tk[2ks+1] (vb); va[mt] / va[4+mt] = rows g / g+8
+      auto vgather = [&](int ks, uint32_t (&va)[8], uint32_t (&vb)[8]) {
+        TokGather ta, tb;
+        const uint32_t sx = 15u - 2u * (uint32_t)g;
+        tok_prep(ta, vbm[2 * ks], ypv + 4u * (uint32_t)(tk[2 * ks] * p.swv), sx);
+        tok_prep(tb, vbm[2 * ks + 1], ypv + 4u * (uint32_t)(tk[2 * ks + 1] * p.swv), sx);
+        va[0] = gather_v<0, 0>(ta); va[4] = gather_v<0, 1>(ta); vb[0] = gather_v<0, 0>(tb); vb[4] = gather_v<0, 1>(tb);
+        va[1] = gather_v<1, 0>(ta); va[5] = gather_v<1, 1>(ta); vb[1] = gather_v<1, 0>(tb); vb[5] = gather_v<1, 1>(tb);
+        va[2] = gather_v<2, 0>(ta); va[6] = gather_v<2, 1>(ta); vb[2] = gather_v<2, 0>(tb); vb[6] = gather_v<2, 1>(tb);
+        va[3] = gather_v<3, 0>(ta); va[7] = gather_v<3, 1>(ta); vb[3] = gather_v<3, 0>(tb); vb[7] = gather_v<3, 1>(tb);
+      };
       // V k-step 0 gathers are issued before the softmax (they do not depend on it), so their
       // shared-memory latency overlaps the shuffles and exp2 of the softmax
       uint32_t va0[8], vb0[8];
-      {
-        float sc[4];
-        uint32_t k0[16], k1[16];
-        gather16(kw0, ypk + 4u * ((uint32_t)(g * p.swk) + (ek & 0xFFFFu)), k0);
-        gather16(kw1, ypk + 4u * ((uint32_t)((g + 8) * p.swk) + (ek >> 16)), k1);
-        scores(sc, k0, k1);
-        gather8x2(hw[0] | (hw[1] << 16), ypv + 4u * ((uint32_t)(tk[0] * p.swv) + (ev & 0xFFu)),
-                  ypv + 4u * ((uint32_t)(tk[1] * p.swv) + ((ev >> 8) & 0xFFu)), va0, vb0);
-        softmax(sc, g < nvalid, g + 8 < nvalid, bb);
-      }
+      vgather(0, va0, vb0);
+      softmax(sc, g < nvalid, g + 8 < nvalid, bb);
       values_ks(0, va0, vb0, bb);
       {
         uint32_t va[8], vb[8];
-        gather8x2(hw[2] | (hw[3] << 16), ypv + 4u * ((uint32_t)(tk[2] * p.swv) + ((ev >> 16) & 0xFFu)),
-                  ypv + 4u * ((uint32_t)(tk[3] * p.swv) + (ev >> 24)), va, vb);
+        vgather(1, va, vb);
         values_ks(1, va, vb, bb);
       }
     }
@@ -683,12 +698,10 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
           for (int nt = 0; nt < 2; ++nt) {
             const int tok = g + 8 * nt;
             if (ok(tok)) {
-              const uint4* pp = reinterpret_cast<const uint4*>(wk + (size_t)(row0 + tok) * kD + 32 * t);
+              // slot j = 2s + hh: channels 16s + 8hh + 2t, +1 = word 4j + t of the row
+              const uint32_t* pp = reinterpret_cast<const uint32_t*>(wk + (size_t)(row0 + tok) * kD) + t;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint4 a = __ldcg(pp + i);
-                kk[nt][4 * i] = a.x; kk[nt][4 * i + 1] = a.y; kk[nt][4 * i + 2] = a.z; kk[nt][4 * i + 3] = a.w;
-              }
+              for (int i = 0; i < 16; ++i) kk[nt][i] = __ldcg(pp + 4 * i);
             } else {
 #pragma unroll
               for (int i = 0; i < 16; ++i) kk[nt][i] = 0u;
@@ -704,10 +717,13 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
           for (int e = 0; e < 2; ++e) {
             const int xx = 2 * ks + e;
             if (ok(tk[xx])) {
-              const uint4* pp = reinterpret_cast<const uint4*>(wv + (size_t)(row0 + tk[xx]) * kD + 16 * g);
-              const uint4 a = __ldcg(pp), b2 = __ldcg(pp + 1);
-              vv[e][0] = a.x; vv[e][1] = a.y; vv[e][2] = a.z; vv[e][3] = a.w;
-              vv[e][4] = b2.x; vv[e][5] = b2.y; vv[e][6] = b2.z; vv[e][7] = b2.w;
+              // rows g / g + 8 of m-tile mt: pair 16mt + g / 16mt + 8 + g = word of the row
+              const uint32_t* pp = reinterpret_cast<const uint32_t*>(wv + (size_t)(row0 + tk[xx]) * kD) + g;
+#pragma unroll
+              for (int mt = 0; mt < 4; ++mt) {
+                vv[e][mt] = __ldcg(pp + 16 * mt);
+                vv[e][4 + mt] = __ldcg(pp + 16 * mt + 8);
+              }
             } else {
 #pragma unroll
               for (int i = 0; i < 8; ++i) vv[e][i] = 0u;
@@ -732,7 +748,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       if (2 * t + 1 < p.G && (G8 || t < 2)) *reinterpret_cast<float2*>(p.ws_ml + (slot * p.G + 2 * t + 1) * 2) = make_float2(m1, lt1);
     }
     // accumulators of tile nt: heads hA = 2(t & 1) + 4 nt (c0, c2), hA + 1 (c1, c3), parity t >> 1;
-    // rows g: channel 16g + 2mt + par, rows g+8: 16g + 8 + 2mt + par
+    // rows g: pair 16mt + g (channel 32mt + 2g + par), rows g+8: pair 16mt + 8 + g
     const int pp_ = t >> 1;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -741,11 +757,11 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       for (int e = 0; e < 2; ++e) {
         const int h = hA + e;
         if (h < p.G) {
-          float* o = p.ws_o + (slot * p.G + h) * kD + 16 * g + pp_;
+          float* o = p.ws_o + (slot * p.G + h) * kD + 2 * g + pp_;
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) {
-            o[2 * mt] = acc[nt][mt][e];
-            o[8 + 2 * mt] = acc[nt][mt][2 + e];
+            o[32 * mt] = acc[nt][mt][e];
+            o[32 * mt + 16] = acc[nt][mt][2 + e];
           }
         }
       }
@@ -931,12 +947,14 @@ size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count) {
 
 bool warp_kernel_supported(int32_t G) { return G >= 1 && G <= 8; }
 
-static int pair_sw(int kp) { return kp + 2; }  // words per token: Y[0..kp]; 2 mod 4 (conflict-free build)
+// words per token: Y[0..kp]; 4 mod 8 for conflict-free 16-byte build stores (MSTF_B128), else 2 mod 4
+// with the V region one word off a 32-word boundary (conflict-free 4-byte stores)
+static int pair_sw(int kp) { return MSTF_B128 ? kp + 4 : kp + 2; }
 
 int warp_region_bytes(int32_t kpk, int32_t kpv, int32_t rqk, int32_t rqv, int* stage_bytes) {
   const int st = 16 * (16 + rqk) + 16 * (16 + rqv);
   if (stage_bytes) *stage_bytes = st;
-  const int pairs = (64 * pair_sw(kpk) + 127) / 128 * 128 + 4 + 64 * pair_sw(kpv);
+  const int pairs = (64 * pair_sw(kpk) + 127) / 128 * 128 + (MSTF_B128 ? 0 : 4) + 64 * pair_sw(kpv);
   return (kWNst * st + (pairs + 7) / 8 * 8 + 8 * kWNst + 127) / 128 * 128;
 }
 
