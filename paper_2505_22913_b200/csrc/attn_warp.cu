@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   constexpr int NT = G8 ? 2 : 1;  // 4-head tiles of the V product
   uint32_t qf[16];                // B operand of the score MMAs: q[head][32t .. 32t+31]
   float acc[NT][4][4];            // O'[pair][(head, parity)] per V n-tile, 4 m-tiles
-  float m0, m1, l0, l1;           // softmax state of heads 2t, 2t+1 (log2 domain)
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // softmax state of heads 2t, 2t+1 (log2 domain)
   const uint32_t par = (uint32_t)(g >> 2);
   const uint32_t sel_lo = par ? 0x1044u : 0x4410u, sel_hi = par ? 0x3244u : 0x4432u;
   // build role of this lane: token lane & 15 of K (lanes 0-15) or V (16-31)
@@ -967,8 +967,10 @@ WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t k
   if (wmax > wcap) wmax = wcap;
   if (wmax < 1) wmax = 1;
   // >= ~4 cost units per worker (each worker pays a segment prologue and writes a partial)
-  int64_t qmin = 4;
-  if (const char* e = std::getenv("MSTF_QMIN")) qmin = std::max(1, std::atoi(e));  // dev A/B
+  // dev A/B knobs, read once (no per-call environment lookups on the launch path)
+  static const int64_t s_qmin = std::getenv("MSTF_QMIN") ? std::max(1, std::atoi(std::getenv("MSTF_QMIN"))) : 4;
+  static const int s_wpc = std::getenv("MSTF_WPC") ? std::atoi(std::getenv("MSTF_WPC")) : 0;
+  const int64_t qmin = s_qmin;
   int64_t workers = (total_cost + qmin - 1) / qmin;
   if (workers < 1) workers = 1;
   int grid = sm_count, wpc = wmax;
@@ -977,10 +979,7 @@ WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t k
     if (wpc > wmax) wpc = wmax;
     if ((int64_t)grid * wpc > workers) grid = (int)std::max<int64_t>(1, (workers + wpc - 1) / wpc);
   }
-  if (const char* e = std::getenv("MSTF_WPC")) {  // dev A/B: warps per CTA
-    const int v = std::atoi(e);
-    if (v >= 1 && v <= wmax) wpc = v;
-  }
+  if (s_wpc >= 1 && s_wpc <= wmax) wpc = s_wpc;  // dev A/B: warps per CTA
   pl.grid = grid;
   pl.wpc = wpc;
   pl.warp_bytes = wb;
