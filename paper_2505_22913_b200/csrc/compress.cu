@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint
   const uint32_t put3 = (0x4444u & ~(0xFu << (4 * q))) | (3u << (4 * q));
   const uint32_t put2 = (0x4444u & ~(0xFu << (4 * q))) | (2u << (4 * q));
   const uint32_t take = 0x4440u | (uint32_t)q;
+  __shared__ __align__(16) uint16_t s_rec[8][4][kD];  // per warp and token slot: the packed record
   for (int row = blockIdx.y; row < 2 * c.U; row += gridDim.y) {
     const int x = row >= c.U;  // 0 = K, 1 = V
     const int u = row - x * c.U;
@@ -233,21 +234,28 @@ __global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint
       }
       pos -= pc;
       const uint32_t hi16 = shfl_down8(m16, 1);
+      // packed values: staged in shared memory (the token's record, slots [0, k) values in channel
+      // order and [k, kpad) zero padding, R7), then written with 16-byte stores
+      uint16_t* sr = s_rec[threadIdx.x >> 5][q];
+      {
+        uint32_t p = pos;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if ((m16 >> (2 * i)) & 1u) sr[p++] = (uint16_t)(w[i] & 0xFFFFu);
+          if ((m16 >> (2 * i + 1)) & 1u) sr[p++] = (uint16_t)(w[i] >> 16);
+        }
+        if (r == 7)
+          for (int j = (int)kk; j < z.kpad; ++j) sr[j] = 0;
+      }
+      __syncwarp();
       if (valid && t < nc) {
         const size_t rec = (size_t)u * c.cap + t;
         if ((r & 1) == 0) reinterpret_cast<uint32_t*>(z.bm + rec * kTiles)[r >> 1] = m16 | (hi16 << 16);
         if ((r & 3) == 0) z.off[rec * kTiles + (r >> 2)] = (uint32_t)t * (uint32_t)z.kpad + pos;
-        uint16_t* vo = z.val + rec * z.kpad;
-        uint32_t p = pos;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if ((m16 >> (2 * i)) & 1u) vo[p++] = (uint16_t)(w[i] & 0xFFFFu);
-          if ((m16 >> (2 * i + 1)) & 1u) vo[p++] = (uint16_t)(w[i] >> 16);
-        }
-        if (r == 7) {
-          for (int j = (int)kk; j < z.kpad; ++j) vo[j] = 0;  // zero padding (R7)
-        }
+        uint4* vo = reinterpret_cast<uint4*>(z.val + rec * z.kpad);
+        for (int j = r; j < z.kpad / 8; j += 8) vo[j] = reinterpret_cast<const uint4*>(sr)[j];
       }
+      __syncwarp();  // the stage is rewritten by the next group
     }
   }
 }
