@@ -278,6 +278,14 @@ int mstf_query_abs_sum(const void* q, int32_t units, int32_t slots, int32_t grou
  * Errors: EINVAL (null / misaligned), ECUDA.                                                 */
 int mstf_dev_read_bandwidth(const void* src, size_t bytes, void* sink, void* stream);
 
+/* Development only: buf (DEVICE u64, or NULL to switch off) receives global-timer stamps (ns)
+ * of the attention kernel's phases: [worker][8] with worker = CTA * warps-per-CTA + warp (0:
+ * start, 1: after the fused appends, 2: first compressed block landed, 3: done) and, from index
+ * 65536, [combine CTA][8] (0: start, 1: done). The caller sizes buf (>= 65536 + U entries x 8)
+ * and keeps it alive while set. Only builds with -DMSTF_TRACE=1 record (the stamps are compiled
+ * out otherwise). Errors: ENOTSUP (not a trace build), ECUDA.                                */
+int mstf_dev_trace(void* buf);
+
 /* Human-readable status (static string). */
 const char* mstf_status_string(int32_t status);
 

@@ -402,6 +402,11 @@ int mstf_dev_read_bandwidth(const void* src, size_t bytes, void* sink, void* str
                  cudaSuccess ? MSTF_OK : MSTF_ECUDA;
 }
 
+int mstf_dev_trace(void* buf) {
+  const cudaError_t e = set_dev_trace(buf);
+  return e == cudaSuccess ? MSTF_OK : e == cudaErrorNotSupported ? MSTF_ENOTSUP : MSTF_ECUDA;
+}
+
 const char* mstf_build_info(void) { return "mustafar-b200 sm_100a (warp-per-worker stream-K, cp.async.bulk + mbarrier, mma.sync m16n8k16, movmatrix)"; }
 
 }  // extern "C"

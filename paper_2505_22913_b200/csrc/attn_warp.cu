@@ -50,7 +50,8 @@ namespace {
 #endif
 constexpr int kWNst = 2;          // TMA ring depth per warp (blocks in flight)
 constexpr int kWMaxWarps = 16;    // warps per CTA (one CTA per SM, <= 128 registers per thread)
-constexpr int kWHdrInts = 16;     // workspace header: [0] S (total cost), [1] cost per unit (0: ragged)
+constexpr int kWHdrInts = 16;
+constexpr int kCombBatch = 16;  // combine: partial slots per sub-warp batch (loads in flight)     // workspace header: [0] S (total cost), [1] cost per unit (0: ragged)
 
 struct WParams {
   CacheView c;
@@ -81,6 +82,29 @@ struct WParams {
   float* part_o;
 };
 
+// Development trace (mstf_dev_trace): per worker, global-timer stamps of its phases; null
+// (the default) compiles to one predicated-off branch per phase.
+// Compiled in only with -DMSTF_TRACE=1 (dev builds: MSTF_NVCC_EXTRA); otherwise the stamps are
+// empty functions and mstf_dev_trace returns MSTF_ENOTSUP.
+#ifndef MSTF_TRACE
+#define MSTF_TRACE 0
+#endif
+__device__ unsigned long long* g_mstf_trace = nullptr;
+constexpr int kTraceSlots = 8;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_at(int worker, int k) {
+#if MSTF_TRACE
+  unsigned long long* tr = g_mstf_trace;
+  if (tr) tr[(size_t)worker * kTraceSlots + k] = gtimer();
+#else
+  (void)worker;
+  (void)k;
+#endif
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -361,6 +385,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   __syncwarp();
   pdl_launch_dependents();
   pdl_wait();  // cache, counters, q and the ragged prefix come from earlier kernels in the stream
+  if (lane == 0) trace_at(P, 0);
 
   // ---- partition (device counters: graph-replay safe)
   int cpu = 0;  // cost per unit (uniform caches)
@@ -388,6 +413,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ready + u), "r"(1) : "memory");
     }
   }
+  if (lane == 0) trace_at(P, 1);
   if (x0 >= x1) return;
 
   // ---- block streams: producer (TMA issue, one block ahead) and consumer walk the same
@@ -606,6 +632,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       const int s = cseq & (kWNst - 1);
       const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes);
       mbar_wait_u32(bar0 + 8 * s, (uint32_t)(cseq / kWNst) & 1u);
+      if (cseq == 0 && lane == 0) trace_at(P, 2);
       const int nvalid = min(16, cn.nc - b * 16);
       if constexpr (Q4)
         build_token_q4<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
@@ -767,6 +794,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       }
     }
   }
+  if (lane == 0) trace_at(P, 3);
 }
 
 // Ragged caches: cost prefix over the units from the device counters (one CTA).
@@ -815,6 +843,7 @@ template <bool SUB>
 __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p) {
   pdl_launch_dependents();
   pdl_wait();  // partials and the plan header come from the attention kernel just before
+  if (threadIdx.x == 0) trace_at(65536 + blockIdx.x, 0);
   extern __shared__ __align__(16) float s_comb[];
   const int G = p.G;
   const int u = blockIdx.x, wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -829,7 +858,7 @@ __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p)
   float m_max = -INFINITY, l_sum = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (h < G) {
-    constexpr int kB = 16;  // slots per batch: all their loads are issued before any math
+    constexpr int kB = kCombBatch;  // slots per batch: all their loads are issued before any math
     for (int i0 = i_lo; i0 < i_hi; i0 += kB) {
       const int cnt = min(kB, i_hi - i0);
       float2 ml = make_float2(-INFINITY, 0.f);
@@ -900,6 +929,7 @@ __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p)
       }
     }
   }
+  if (threadIdx.x == 0) trace_at(65536 + blockIdx.x, 1);
   if (p.fuse && threadIdx.x == 0) {  // a4 bookkeeping of the fused step (after every reader)
     const int nc = p.c.n_comp[u], nw = p.c.n_win[u];
     if (p.c.W == 0 || nw == p.c.W) p.c.n_comp[u] = nc + 1; else p.c.n_win[u] = nw + 1;
@@ -946,6 +976,12 @@ size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count) {
 }
 
 bool warp_kernel_supported(int32_t G) { return G >= 1 && G <= 8; }
+
+cudaError_t set_dev_trace(void* buf) {
+  if (!MSTF_TRACE) return cudaErrorNotSupported;
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  return cudaMemcpyToSymbol(g_mstf_trace, &p, sizeof(p));
+}
 
 // words per token: Y[0..kp]; 4 mod 8 for conflict-free 16-byte build stores (MSTF_B128), else 2 mod 4
 // with the V region one word off a 32-word boundary (conflict-free 4-byte stores)
@@ -1054,7 +1090,7 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   if (e != cudaSuccess) return e;
   // combine: sub-warps per head when a unit has many partial slots (few units)
   const int64_t slots_per_unit = ((int64_t)p.np + c.U - 1) / c.U + 2;
-  int sub = (int)((slots_per_unit + 15) / 16);
+  int sub = (int)((slots_per_unit + kCombBatch - 1) / kCombBatch);
   sub = std::max(1, std::min(std::min(sub, 4), 512 / (32 * G)));
   if (sub == 1) return launch_pdl(mstf_warp_combine_kernel<false>, dim3(c.U), dim3(32 * G), 0, s, p);
   const size_t csmem = (size_t)(sub - 1) * G * (kD * sizeof(float) + sizeof(float2));

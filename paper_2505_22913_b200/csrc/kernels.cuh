@@ -85,6 +85,7 @@ struct WarpPlan {
   int32_t smem;        // dynamic shared memory per CTA
 };
 bool warp_kernel_supported(int32_t G);
+cudaError_t set_dev_trace(void* buf);  // development: per-worker phase stamps (null: off)
 size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count);
 int warp_region_bytes(int32_t kpk, int32_t kpv, int32_t rqk, int32_t rqv, int* stage_bytes);
 WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t kpk, int32_t kpv, int32_t rqk,

@@ -31,7 +31,7 @@ EXPORTS = ("mstf_keep_from_sparsity", "mstf_k_pad", "mstf_value_record_bytes", "
            "mstf_decode_step_kernel_count", "mstf_attention_kernel_count",
            "mstf_set_key_weights", "mstf_query_abs_sum",
            "mstf_seq_split", "mstf_sparse_decode_attention_partial", "mstf_merge_partials",
-           "mstf_dev_read_bandwidth", "mstf_graph_step_check", "mstf_graph_step_commit",
+           "mstf_dev_read_bandwidth", "mstf_dev_trace", "mstf_graph_step_check", "mstf_graph_step_commit",
            "mstf_status_string", "mstf_build_info")
 
 
@@ -84,13 +84,19 @@ def lib() -> ctypes.CDLL:
         "mstf_sparse_decode_attention_partial": (ctypes.c_int, [vp, vp, ctypes.c_float, vp, vp, vp, sz, vp]),
         "mstf_merge_partials": (ctypes.c_int, [i32, i32, i32, i32, vp, vp, vp, i32, vp]),
         "mstf_dev_read_bandwidth": (ctypes.c_int, [vp, sz, vp, vp]),
+        "mstf_dev_trace": (ctypes.c_int, [vp]),
         "mstf_graph_step_check": (ctypes.c_int, [vp, i32]),
         "mstf_graph_step_commit": (ctypes.c_int, [vp, i32]),
         "mstf_status_string": (ctypes.c_char_p, [i32]),
         "mstf_build_info": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
-        f = getattr(L, name)
+        try:
+            f = getattr(L, name)
+        except AttributeError:
+            if name.startswith("mstf_dev_"):  # development hooks: optional (A/B of older builds)
+                continue
+            raise
         f.restype, f.argtypes = res, args
     _lib = L
     return L
@@ -179,6 +185,14 @@ def dev_read_bandwidth(x: torch.Tensor, sink: torch.Tensor, stream=None):
     _check("mstf_dev_read_bandwidth", lib().mstf_dev_read_bandwidth(x.data_ptr(), x.numel() * x.element_size(),
                                                                     _dev_ptr(sink, torch.int32, "sink"),
                                                                     _stream(stream)))
+
+
+def dev_trace(buf: torch.Tensor | None):
+    """Development only: record the attention kernel's per-worker phase stamps into buf (int64
+    CUDA tensor, >= (65536 + units) x 8 entries), or stop recording (None)."""
+    if buf is not None and (not buf.is_cuda or buf.dtype != torch.int64 or not buf.is_contiguous()):
+        raise ValueError("buf must be a contiguous int64 CUDA tensor")
+    _check("mstf_dev_trace", lib().mstf_dev_trace(None if buf is None else buf.data_ptr()))
 
 
 def buffer_bytes(cfg: Config):
