@@ -58,6 +58,7 @@ struct WParams {
   const uint16_t* q;      // [U][G][kD]
   int G;
   float scale_log2;
+  float lazy_log2;        // softmax reference-max slack (log2 units; 0: exact running max)
   int np;                 // workers (warps of the grid)
   int wpc;                // warps per CTA
   int cs, cw;             // cost model: per-segment start, per window block
@@ -526,11 +527,11 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     const float x0 = vg ? sc[0] * p.scale_log2 : -INFINITY, x1 = vg ? sc[1] * p.scale_log2 : -INFINITY;
     const float x2 = vg8 ? sc[2] * p.scale_log2 : -INFINITY, x3 = vg8 ? sc[3] * p.scale_log2 : -INFINITY;
     // Lazy rescale: the running reference max m moves only when a score exceeds it by more than
-    // kLazyLog2 (then P <= 2^kLazyLog2 in fp16, exact to its 11 bits; l and o are fp32, and the
+    // p.lazy_log2 = 8 (then P <= 2^8, still rounded to fp16 as always; l and o are fp32, and the
     // combine merges slots by their own m, so any reference value is exact algebra). The common
-    // case skips the max reduction and the accumulator rescale.
-    constexpr float kLazyLog2 = 8.f;
-    const bool need = fmaxf(fmaxf(x0, x2) - m0, fmaxf(x1, x3) - m1) > kLazyLog2;
+    // case skips the max reduction and the accumulator rescale. Partials handed to the caller
+    // (sequence split) use 0: m is then the exact running max, as the ABI states.
+    const bool need = fmaxf(fmaxf(x0, x2) - m0, fmaxf(x1, x3) - m1) > p.lazy_log2;
     if (__any_sync(0xffffffffu, need)) {
       float b0 = fmaxf(x0, x2), b1 = fmaxf(x1, x3);
 #pragma unroll
@@ -1032,6 +1033,9 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   p.q = q;
   p.G = G;
   p.scale_log2 = scale * 1.4426950408889634f;
+  // lazy rescale (reference max within 8 of the true max) for the normalised output; the exact
+  // running max when the caller receives the partials themselves (m = max, the ABI contract)
+  p.lazy_log2 = part_ml ? 0.f : 8.f;
   p.np = plan.grid * plan.wpc;
   p.wpc = plan.wpc;
   sk_cost_params(&p.cs, &p.cw);

@@ -41,4 +41,18 @@ res = {"B": B, "T": T, "fused": fused, "workers": int(act.sum()),
        "done_us": [round(float(rel[:, 3][w[:, 3] > 0].min()), 2), round(float(rel[:, 3][w[:, 3] > 0].median()), 2), round(float(rel[:, 3][w[:, 3] > 0].max()), 2)],
        "combine_start_us": [round(float(((comb[:, 0] - t0) / 1e3).min()), 2), round(float(((comb[:, 0] - t0) / 1e3).max()), 2)] if len(comb) else None,
        "combine_done_us": [round(float(((comb[:, 1] - t0) / 1e3).min()), 2), round(float(((comb[:, 1] - t0) / 1e3).max()), 2)] if len(comb) else None}
+# per-CTA spread (workers = CTA * wpc + warp; wpc from the number of active workers / 148 if full)
+wpc = int(sys.argv[4]) if len(sys.argv) > 4 else 16
+d = (tr[:65536, 3].double() - t0) / 1e3
+act_all = tr[:65536, 0] > 0
+nw = int(act_all.sum())
+if nw % wpc == 0 and nw // wpc <= 148:
+    dd = d[:nw].view(nw // wpc, wpc)
+    cta_max = dd.max(1).values
+    cta_min = dd.min(1).values
+    res["cta_done_max_us"] = [round(float(cta_max.min()), 2), round(float(cta_max.median()), 2), round(float(cta_max.max()), 2)]
+    res["within_cta_spread_us_median"] = round(float((cta_max - cta_min).median()), 2)
+    res["done_by_warp_idx_mean_us"] = [round(float(x), 1) for x in dd.mean(0)]
+    fb = (tr[:nw, 2].double() - t0) / 1e3
+    res["first_block_by_warp_idx_mean_us"] = [round(float(x), 2) for x in fb.view(nw // wpc, wpc).mean(0)]
 print(json.dumps(res), flush=True)
