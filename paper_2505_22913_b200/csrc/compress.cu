@@ -58,7 +58,9 @@ __global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint
   const uint32_t put3 = (0x4444u & ~(0xFu << (4 * q))) | (3u << (4 * q));
   const uint32_t put2 = (0x4444u & ~(0xFu << (4 * q))) | (2u << (4 * q));
   const uint32_t take = 0x4440u | (uint32_t)q;
-  __shared__ __align__(16) uint16_t s_rec[8][4][kD];  // per warp and token slot: the packed record
+  // per warp and token slot: the packed record; rows of kD + 8 halves (66 words: the four token
+  // slots of a warp start in different banks, so their 2-byte stores do not conflict)
+  __shared__ __align__(16) uint16_t s_rec[8][4][kD + 8];
   for (int row = blockIdx.y; row < 2 * c.U; row += gridDim.y) {
     const int x = row >= c.U;  // 0 = K, 1 = V
     const int u = row - x * c.U;
