@@ -696,6 +696,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
         vgather(1, va, vb);
         values_ks(1, va, vb, bb);
       }
+      __syncwarp();  // every lane's gathers precede the next block's pair-array builds (WAR)
     }
 
     // -------- window blocks [max(lo, nbc), hi): dense ring rows (a6)
