@@ -51,6 +51,7 @@ namespace {
 constexpr int kWNst = 2;          // TMA ring depth per warp (blocks in flight)
 constexpr int kWMaxWarps = 16;    // warps per CTA (one CTA per SM, <= 128 registers per thread)
 constexpr int kWHdrInts = 16;
+constexpr int kWPartBytes = 4 * 128 * 4 + 4 * 2 * 4;  // a warp's partial in shared memory (G <= 4)
 constexpr int kCombBatch = 16;  // combine: partial slots per sub-warp batch (loads in flight)     // workspace header: [0] S (total cost), [1] cost per unit (0: ragged)
 
 struct WParams {
@@ -74,6 +75,10 @@ struct WParams {
   int* pref;              // [U+1] ragged cost prefix (written by mstf_cost_prefix_kernel)
   float* ws_o;            // [slots][G][kD] partial o (unnormalised)
   float* ws_ml;           // [slots][G][2] partial (m, l), log2 domain
+  int cta_merge;          // small problems (<= 1 cost unit per warp, G <= 4): warp partials stay in
+                          // shared memory and the CTA writes one partial per unit (slot CTA + u of ws2)
+  float* ws2_o;           // [grid + U + 1][G][kD]
+  float* ws2_ml;          // [grid + U + 1][G][2]
   const uint16_t* k_new;  // fused step: [U][kD]
   const uint16_t* v_new;
   // combine
@@ -354,11 +359,12 @@ __device__ __forceinline__ int worker_begin(long long S, int np, int P) { return
 
 // Fused step: wait until the unit's append is published (bounded spin: a broken invariant
 // becomes a launch error, not a hung GPU).
+// ready[u] counts the unit's appended tensors (K and V may be appended by different workers).
 __device__ __forceinline__ void wait_ready(const int* flag) {
   int v;
   for (uint32_t it = 0;; ++it) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if (v != 0) break;
+    if (v >= 2) break;
     if (it > (1u << 22)) __trap();
     __nanosleep(64);
   }
@@ -377,7 +383,9 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   const uint32_t wbase = smem_u32(smem) + (uint32_t)(warp * p.warp_bytes);
   const uint32_t ypk = wbase + (uint32_t)(kWNst * p.stage_bytes);  // 128-byte aligned
   const uint32_t ypv = ypk + ((64u * (uint32_t)p.swk + 127u) & ~127u) + (MSTF_B128 ? 0u : 4u);
-  const uint32_t bar0 = (ypv + 64u * (uint32_t)p.swv + 7u) & ~7u;
+  const uint32_t bar0 = (max(ypv + 64u * (uint32_t)p.swv, ypk + (uint32_t)kWPartBytes) + 7u) & ~7u;
+  __shared__ int s_wunit[kWMaxWarps];  // cta_merge: the unit of the warp's partial (-1: none)
+  if (lane == 0) s_wunit[warp] = -1;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kWNst; ++s) mbar_init_u32(bar0 + 8 * s, 1);
@@ -403,19 +411,25 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   }
   const int x0 = worker_begin(S, p.np, P), x1 = worker_begin(S, p.np, P + 1);
 
-  // ---- a4 (fused step): append the units whose first cost unit this worker owns
+  // ---- a4 (fused step): tensor x (0: K, 1: V) of unit u is appended by the owner of the unit's
+  // start cost unit min(x, cs - 1) -- with cs >= 2 two workers when the partition splits them
+  // (small problems: two otherwise idle warps), one worker doing both otherwise
   if (p.fuse) {
-    for (int u = (x0 + cpu - 1) / cpu; u < c.U && u * cpu < x1; ++u) {
-      const int nc0 = c.n_comp[u], nw0 = c.n_win[u];
-      append_unit_warp(c, 0, u, p.k_new + (size_t)u * kD, nc0, nw0, lane);
-      append_unit_warp(c, 1, u, p.v_new + (size_t)u * kD, nc0, nw0, lane);
-      __syncwarp();
-      __threadfence();
-      if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.ready + u), "r"(1) : "memory");
+    for (int u = max(0, x0 / cpu - 1); u < c.U && u * cpu < x1; ++u) {
+      for (int x = 0; x < 2; ++x) {
+        const int j = u * cpu + min(x, p.cs - 1);
+        if (j < x0 || j >= x1) continue;
+        const int nc0 = c.n_comp[u], nw0 = c.n_win[u];
+        append_unit_warp(c, x, u, (x ? p.v_new : p.k_new) + (size_t)u * kD, nc0, nw0, lane);
+        __syncwarp();
+        __threadfence();
+        if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + u), "r"(1) : "memory");
+      }
     }
   }
   if (lane == 0) trace_at(P, 1);
-  if (x0 >= x1) return;
+  if (x0 >= x1 && !p.cta_merge) return;
+  if (x0 < x1) {  // (cta_merge: every warp reaches the CTA merge at the end)
 
   // ---- block streams: producer (TMA issue, one block ahead) and consumer walk the same
   // sequence of compressed blocks: segment by segment, unit u's blocks [lo, min(hi, nbc)).
@@ -763,8 +777,16 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       }
     }
 
-    // -------- segment partial (slot P + u): m, l (log2 domain), o unnormalised
+    // -------- segment partial (slot P + u): m, l (log2 domain), o unnormalised; cta_merge: the
+    // warp's one partial goes to its pair-array region (free after its last block)
     const size_t slot = (size_t)P + u;
+    float* dml = p.ws_ml + slot * p.G * 2;
+    float* dO = p.ws_o + slot * p.G * kD;
+    if (p.cta_merge) {
+      dO = reinterpret_cast<float*>(smem + (ypk - smem_u32(smem)));
+      dml = dO + p.G * kD;
+      if (lane == 0) s_wunit[warp] = u;
+    }
     float lt0 = l0, lt1 = l1;
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
@@ -773,8 +795,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     }
     // lanes g = 0: heads 2t, 2t+1 (G <= 4: t < 2 are the real heads; G = 8: every t)
     if (g == 0) {
-      if (2 * t < p.G && (G8 || t < 2)) *reinterpret_cast<float2*>(p.ws_ml + (slot * p.G + 2 * t) * 2) = make_float2(m0, lt0);
-      if (2 * t + 1 < p.G && (G8 || t < 2)) *reinterpret_cast<float2*>(p.ws_ml + (slot * p.G + 2 * t + 1) * 2) = make_float2(m1, lt1);
+      if (2 * t < p.G && (G8 || t < 2)) *reinterpret_cast<float2*>(dml + (2 * t) * 2) = make_float2(m0, lt0);
+      if (2 * t + 1 < p.G && (G8 || t < 2)) *reinterpret_cast<float2*>(dml + (2 * t + 1) * 2) = make_float2(m1, lt1);
     }
     // accumulators of tile nt: heads hA = 2(t & 1) + 4 nt (c0, c2), hA + 1 (c1, c3), parity t >> 1;
     // rows g: pair 16mt + g (channel 32mt + 2g + par), rows g+8: pair 16mt + 8 + g
@@ -786,7 +808,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       for (int e = 0; e < 2; ++e) {
         const int h = hA + e;
         if (h < p.G) {
-          float* o = p.ws_o + (slot * p.G + h) * kD + 2 * g + pp_;
+          float* o = dO + h * kD + 2 * g + pp_;
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) {
             o[32 * mt] = acc[nt][mt][e];
@@ -796,7 +818,54 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       }
     }
   }
+  }  // x0 < x1
   if (lane == 0) trace_at(P, 3);
+  if (p.cta_merge) {
+    // merge the CTA's warp partials per unit (shared memory) into one partial (slot CTA + u of ws2)
+    __syncthreads();
+    const int cb = (int)blockIdx.x, wpc = p.wpc;
+    const int X0 = worker_begin(S, p.np, cb * wpc), X1 = worker_begin(S, p.np, (cb + 1) * wpc);
+    if (X0 < X1) {
+      const int uA = unit_of_cost(p, X0, cpu), uB = unit_of_cost(p, X1 - 1, cpu);
+      const uint32_t wb = (uint32_t)p.warp_bytes / 4;
+      const float* so0 = reinterpret_cast<const float*>(smem + (ypk - smem_u32(smem))) - warp * wb;  // warp 0's
+      int wu[kWMaxWarps];  // the unit of each warp's partial (-1: none), in registers
+#pragma unroll
+      for (int w = 0; w < kWMaxWarps; ++w) wu[w] = w < wpc ? s_wunit[w] : -1;
+      for (int u = uA; u <= uB; ++u) {
+        for (int i = threadIdx.x; i < p.G * kD; i += blockDim.x) {
+          const int h = i / kD;
+          // all loads independent (unrolled, selects instead of branches): one smem round trip
+          float mw[kWMaxWarps], lw[kWMaxWarps], ow[kWMaxWarps];
+#pragma unroll
+          for (int w = 0; w < kWMaxWarps; ++w) {
+            const float* b2 = so0 + (w < wpc ? w : 0) * wb;
+            const float2 ml = *reinterpret_cast<const float2*>(b2 + p.G * kD + 2 * h);
+            const bool mine = wu[w] == u;  // other regions may hold pair-array bits: select, not scale
+            mw[w] = mine ? ml.x : -INFINITY;
+            lw[w] = mine ? ml.y : 0.f;
+            ow[w] = mine ? b2[i] : 0.f;
+          }
+          float mm = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < kWMaxWarps; ++w) mm = fmaxf(mm, mw[w]);
+          float lsum = 0.f, osum = 0.f;
+          if (mm != -INFINITY) {
+#pragma unroll
+            for (int w = 0; w < kWMaxWarps; ++w) {
+              const float a = mw[w] == -INFINITY ? 0.f : ex2(mw[w] - mm);  // lw = ow = 0 there
+              lsum += a * lw[w];
+              osum += a * ow[w];
+            }
+          }
+          const size_t slot = (size_t)cb + u;
+          p.ws2_o[slot * p.G * kD + i] = osum;
+          if ((i & (kD - 1)) == 0) *reinterpret_cast<float2*>(p.ws2_ml + (slot * p.G + h) * 2) = make_float2(mm, lsum);
+        }
+      }
+    }
+    if (lane == 0) trace_at(P, 4);
+  }
 }
 
 // Ragged caches: cost prefix over the units from the device counters (one CTA).
@@ -854,7 +923,15 @@ __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p)
   const int cpu = p.hdr[1];
   const int us = cpu ? u * cpu : p.pref[u], ue = cpu ? (u + 1) * cpu : p.pref[u + 1];
   // workers overlapping [us, ue): first = owner of us, last = owner of ue - 1
-  const int wf = (int)(((long long)(us + 1) * p.np - 1) / S), wl = (int)(((long long)ue * p.np - 1) / S);
+  int wf = (int)(((long long)(us + 1) * p.np - 1) / S), wl = (int)(((long long)ue * p.np - 1) / S);
+  const float* ws_o = p.ws_o;
+  const float* ws_ml = p.ws_ml;
+  if (p.cta_merge) {  // one partial per CTA (slot CTA + u of ws2)
+    wf /= p.wpc;
+    wl /= p.wpc;
+    ws_o = p.ws2_o;
+    ws_ml = p.ws2_ml;
+  }
   const int np_ = wl - wf + 1;
   const int i_lo = np_ * sub / Sn, i_hi = np_ * (sub + 1) / Sn;
   float m_max = -INFINITY, l_sum = 0.f;
@@ -864,11 +941,11 @@ __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p)
     for (int i0 = i_lo; i0 < i_hi; i0 += kB) {
       const int cnt = min(kB, i_hi - i0);
       float2 ml = make_float2(-INFINITY, 0.f);
-      if (lane < cnt) ml = *reinterpret_cast<const float2*>(p.ws_ml + ((size_t)(wf + i0 + lane + u) * G + h) * 2);
+      if (lane < cnt) ml = *reinterpret_cast<const float2*>(ws_ml + ((size_t)(wf + i0 + lane + u) * G + h) * 2);
       float4 v[kB];
 #pragma unroll
       for (int i = 0; i < kB; ++i)
-        v[i] = i < cnt ? *(reinterpret_cast<const float4*>(p.ws_o + ((size_t)(wf + i0 + i + u) * G + h) * kD) + lane)
+        v[i] = i < cnt ? *(reinterpret_cast<const float4*>(ws_o + ((size_t)(wf + i0 + i + u) * G + h) * kD) + lane)
                        : make_float4(0.f, 0.f, 0.f, 0.f);
       float mb = ml.x;
 #pragma unroll
@@ -972,9 +1049,10 @@ static cudaError_t set_max_smem(void* kern, int bytes) {
 }
 
 size_t warp_ws_bytes(int32_t U, int32_t G, int32_t sm_count) {
-  const size_t slots = (size_t)sm_count * kWMaxWarps + U + 1;
+  const size_t slots = (size_t)sm_count * kWMaxWarps + U + 1, slots2 = (size_t)sm_count + U + 1;
   return r256(kWHdrInts * sizeof(int)) + r256((size_t)U * sizeof(int)) + r256((size_t)(U + 1) * sizeof(int)) +
-         r256(slots * G * 2 * sizeof(float)) + slots * G * kD * sizeof(float);
+         r256(slots * G * 2 * sizeof(float)) + r256(slots * G * kD * sizeof(float)) +
+         r256(slots2 * G * 2 * sizeof(float)) + slots2 * G * kD * sizeof(float);
 }
 
 bool warp_kernel_supported(int32_t G) { return G >= 1 && G <= 8; }
@@ -992,7 +1070,8 @@ static int pair_sw(int kp) { return MSTF_B128 ? kp + 4 : kp + 2; }
 int warp_region_bytes(int32_t kpk, int32_t kpv, int32_t rqk, int32_t rqv, int* stage_bytes) {
   const int st = 16 * (16 + rqk) + 16 * (16 + rqv);
   if (stage_bytes) *stage_bytes = st;
-  const int pairs = (64 * pair_sw(kpk) + 127) / 128 * 128 + (MSTF_B128 ? 0 : 4) + 64 * pair_sw(kpv);
+  int pairs = (64 * pair_sw(kpk) + 127) / 128 * 128 + (MSTF_B128 ? 0 : 4) + 64 * pair_sw(kpv);
+  if (pairs < kWPartBytes) pairs = kWPartBytes;  // the region also holds a warp's partial (cta_merge)
   return (kWNst * st + (pairs + 7) / 8 * 8 + 8 * kWNst + 127) / 128 * 128;
 }
 
@@ -1008,7 +1087,12 @@ WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t k
   // dev A/B knobs, read once (no per-call environment lookups on the launch path)
   static const int64_t s_qmin = std::getenv("MSTF_QMIN") ? std::max(1, std::atoi(std::getenv("MSTF_QMIN"))) : 4;
   static const int s_wpc = std::getenv("MSTF_WPC") ? std::atoi(std::getenv("MSTF_WPC")) : 0;
-  const int64_t qmin = s_qmin;
+  // Small problems (at most one cost unit per warp fills the GPU, G <= 4): one cost unit per
+  // warp, warp partials merged per CTA in shared memory (cta_merge). MSTF_CTAMERGE=0: dev A/B.
+  static const int s_ctam = std::getenv("MSTF_CTAMERGE") ? std::atoi(std::getenv("MSTF_CTAMERGE")) : 1;
+  const bool small = s_ctam != 0 && G <= 4 && total_cost <= (int64_t)sm_count * wmax &&
+                     (total_cost + s_qmin - 1) / s_qmin < (int64_t)sm_count * wmax / 2;
+  const int64_t qmin = small ? 1 : s_qmin;
   int64_t workers = (total_cost + qmin - 1) / qmin;
   if (workers < 1) workers = 1;
   int grid = sm_count, wpc = wmax;
@@ -1020,6 +1104,7 @@ WarpPlan plan_warp_attention(int32_t U, int32_t G, int64_t total_cost, int32_t k
   if (s_wpc >= 1 && s_wpc <= wmax) wpc = s_wpc;  // dev A/B: warps per CTA
   pl.grid = grid;
   pl.wpc = wpc;
+  pl.cta_merge = small && wpc > 1 && (int64_t)grid * wpc >= total_cost ? 1 : 0;
   pl.warp_bytes = wb;
   pl.smem = wpc * wb;
   return pl;
@@ -1064,6 +1149,12 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   p.ws_ml = reinterpret_cast<float*>(w);
   w += r256(slots * G * 2 * sizeof(float));
   p.ws_o = reinterpret_cast<float*>(w);
+  w += r256(slots * G * kD * sizeof(float));
+  const size_t slots2 = (size_t)sm_count + c.U + 1;
+  p.ws2_ml = reinterpret_cast<float*>(w);
+  w += r256(slots2 * G * 2 * sizeof(float));
+  p.ws2_o = reinterpret_cast<float*>(w);
+  p.cta_merge = plan.cta_merge;
   p.k_new = k_new;
   p.v_new = v_new;
   p.out = out;
@@ -1094,9 +1185,11 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   e = launch_pdl(kf, dim3(plan.grid), dim3(32 * plan.wpc), (size_t)plan.smem, s, p);
   if (e != cudaSuccess) return e;
   // combine: sub-warps per head when a unit has many partial slots (few units)
-  const int64_t slots_per_unit = ((int64_t)p.np + c.U - 1) / c.U + 2;
+  const int64_t slots_per_unit = ((int64_t)(p.cta_merge ? plan.grid : p.np) + c.U - 1) / c.U + 2;
   int sub = (int)((slots_per_unit + kCombBatch - 1) / kCombBatch);
-  sub = std::max(1, std::min(std::min(sub, 4), 512 / (32 * G)));
+  // dev A/B knob (read once): cap on the sub-warps per head
+  static const int s_subcap = std::getenv("MSTF_COMBSUB_MAX") ? std::max(1, std::atoi(std::getenv("MSTF_COMBSUB_MAX"))) : 4;
+  sub = std::max(1, std::min(std::min(sub, s_subcap), 512 / (32 * G)));
   if (sub == 1) return launch_pdl(mstf_warp_combine_kernel<false>, dim3(c.U), dim3(32 * G), 0, s, p);
   const size_t csmem = (size_t)(sub - 1) * G * (kD * sizeof(float) + sizeof(float2));
   return launch_pdl(mstf_warp_combine_kernel<true>, dim3(c.U), dim3(32 * G * sub), csmem, s, p);

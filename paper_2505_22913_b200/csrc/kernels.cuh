@@ -81,6 +81,7 @@ cudaError_t launch_dense_attention(const uint16_t* k, const uint16_t* v, const i
 struct WarpPlan {
   int32_t grid;        // CTAs (<= SMs, one per SM)
   int32_t wpc;         // warps (workers) per CTA
+  int32_t cta_merge;   // small problems: warp partials merged per CTA in shared memory
   int32_t warp_bytes;  // shared memory per warp
   int32_t smem;        // dynamic shared memory per CTA
 };

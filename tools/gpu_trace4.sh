@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+MSTF_NVCC_EXTRA="-DMSTF_TRACE=1" python -m paper_2505_22913_b200.build --force > gpurun_out/build_tr.log 2>&1
+for a in "1 4096 nf 15" "1 64 nf 1"; do timeout 300 python tools/trace_attn.py $a >> gpurun_out/trace.txt 2>&1; done

@@ -38,6 +38,7 @@ res = {"B": B, "T": T, "fused": fused, "workers": int(act.sum()),
        "start_us": [round(float(rel[:, 0].min()), 2), round(float(rel[:, 0].median()), 2), round(float(rel[:, 0].max()), 2)],
        "after_append_us": [round(float(rel[:, 1].median()), 2), round(float(rel[:, 1].max()), 2)],
        "first_block_us": [round(float(rel[:, 2][w[:, 2] > 0].min()), 2), round(float(rel[:, 2][w[:, 2] > 0].median()), 2), round(float(rel[:, 2][w[:, 2] > 0].max()), 2)],
+       "merged_us": [round(float(rel[:, 4][w[:, 4] > 0].min()), 2), round(float(rel[:, 4][w[:, 4] > 0].max()), 2)] if bool((w[:, 4] > 0).any()) else None,
        "done_us": [round(float(rel[:, 3][w[:, 3] > 0].min()), 2), round(float(rel[:, 3][w[:, 3] > 0].median()), 2), round(float(rel[:, 3][w[:, 3] > 0].max()), 2)],
        "combine_start_us": [round(float(((comb[:, 0] - t0) / 1e3).min()), 2), round(float(((comb[:, 0] - t0) / 1e3).max()), 2)] if len(comb) else None,
        "combine_done_us": [round(float(((comb[:, 1] - t0) / 1e3).min()), 2), round(float(((comb[:, 1] - t0) / 1e3).max()), 2)] if len(comb) else None}
