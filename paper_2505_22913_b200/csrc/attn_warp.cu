@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   // ---- partition (device counters: graph-replay safe)
   int cpu = 0;  // cost per unit (uniform caches)
   long long S;
+  const int nc_0 = c.n_comp[0], nw_0 = c.n_win[0];  // unit 0's counters (before a fused append)
   if (p.uniform) {
     cpu = cost_of(p, counters_of(p, 0).nc);
     S = (long long)c.U * cpu;
@@ -419,8 +420,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       for (int x = 0; x < 2; ++x) {
         const int j = u * cpu + min(x, p.cs - 1);
         if (j < x0 || j >= x1) continue;
-        const int nc0 = c.n_comp[u], nw0 = c.n_win[u];
-        append_unit_warp(c, x, u, (x ? p.v_new : p.k_new) + (size_t)u * kD, nc0, nw0, lane);
+        // uniform caches (fuse requires it): unit 0's counters, already read for the partition
+        append_unit_warp(c, x, u, (x ? p.v_new : p.k_new) + (size_t)u * kD, nc_0, nw_0, lane);
         __syncwarp();
         __threadfence();
         if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + u), "r"(1) : "memory");

@@ -262,17 +262,19 @@ __device__ __forceinline__ void append_unit_warp(const CacheView& c, int x, int 
   const size_t rec = (size_t)u * c.cap + nc;
   const Sel z = sel_tensor(c, x);
   const float* kw = (x == 0 && c.kw) ? c.kw + (size_t)u * kD : nullptr;
+  const uint2 tok = reinterpret_cast<const uint2*>(src)[lane];  // the new token (load issued first)
   if (c.W == 0) {
-    compress_token_warp(src, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.rec_val(rec),
-                        z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
+    compress_raw_warp(tok, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.rec_val(rec),
+                      z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
   } else if (nw == c.W) {
-    uint16_t* slot = z.win + ((size_t)u * c.W + (nc % c.W)) * kD;
-    compress_token_warp(slot, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.rec_val(rec),
-                        z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
+    uint2* slot = reinterpret_cast<uint2*>(z.win + ((size_t)u * c.W + (nc % c.W)) * kD);
+    const uint2 old = slot[lane];  // the evicted (oldest) window token
+    compress_raw_warp(old, z.keep, z.kpad, (uint32_t)nc, z.bm + rec * kTiles, z.rec_val(rec),
+                      z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
     __syncwarp();
-    copy_token_warp(src, slot, lane);
+    slot[lane] = tok;
   } else {
-    copy_token_warp(src, z.win + ((size_t)u * c.W + ((nc + nw) % c.W)) * kD, lane);
+    reinterpret_cast<uint2*>(z.win + ((size_t)u * c.W + ((nc + nw) % c.W)) * kD)[lane] = tok;
   }
 }
 
