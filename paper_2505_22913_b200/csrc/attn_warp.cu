@@ -422,8 +422,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
         if (j < x0 || j >= x1) continue;
         // uniform caches (fuse requires it): unit 0's counters, already read for the partition
         append_unit_warp(c, x, u, (x ? p.v_new : p.k_new) + (size_t)u * kD, nc_0, nw_0, lane);
-        __syncwarp();
-        __threadfence();
+        __syncwarp();  // orders every lane's record / window stores before lane 0's release
         if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + u), "r"(1) : "memory");
       }
     }
