@@ -2,7 +2,8 @@
 // P:236-261), one self-contained warp per work item: the round-2 kernel.
 //
 // Every warp of a persistent grid (one CTA per SM) is an independent stream-K worker over the
-// concatenated 16-token blocks of all units:
+// concatenated 16-token blocks of all units; small problems give each warp
+// at most one block and merge the warps' partials per CTA in shared memory (cta_merge):
 //   * its compressed blocks are streamed from HBM by TMA bulk copies (cp.async.bulk, four per
 //     block: K bitmaps, K values, V bitmaps, V values -- each a contiguous run of fixed-stride
 //     records, R5-R7) into a private 2-stage shared-memory ring; the warp issues them itself
@@ -26,10 +27,10 @@
 //   * each (worker, unit) segment writes one partial (m, l, o) slot; the combine kernel (a9)
 //     merges a unit's slots.
 //
-// Fused decode step (mstf_decode_step, uniform caches): the worker that owns a unit's first
-// cost unit also appends that unit's new token (a4) before its attention work and publishes
-// a ready flag; a worker reading the unit's last record or its window waits for the flag.
-// The appender's index is never higher than a reader's, so in-order CTA dispatch cannot
+// Fused decode step (mstf_decode_step, uniform caches): the workers that own a unit's two start
+// cost units append its new K and V token (a4) before their attention work and count a ready
+// flag up; a worker reading the unit's last record or its window waits for both. The
+// appenders' indices are never higher than a reader's, so in-order CTA dispatch cannot
 // deadlock. Counters are read from the device and NOT written here (the combine kernel
 // writes the post-append counters and clears the flags), so a captured CUDA graph of the
 // step replays correctly.
