@@ -70,23 +70,7 @@ __global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint
     const Sel z = sel_tensor(c, x);
     const uint32_t kk = (uint32_t)z.keep;
     const int gend = min(g0 + 4 * kPrefillGroups, ntok);
-    if ((x == 0 && c.kw) || c.vbits == 4) {
-      // output-aware K pruning (float32 score keys) or the 4-bit payload (NEXT-4): one
-      // warp per token
-      const float* kw = (x == 0 && c.kw) ? c.kw + (size_t)u * kD : nullptr;
-      const uint16_t* base = (x ? v : k) + (size_t)u * T * kD;
-      for (int t = g0; t < gend; ++t) {
-        const uint2 raw = reinterpret_cast<const uint2*>(base + (size_t)t * kD)[lane];
-        if (t < nc) {
-          const size_t rec = (size_t)u * c.cap + t;
-          compress_raw_warp(raw, z.keep, z.kpad, (uint32_t)t, z.bm + rec * kTiles, z.rec_val(rec),
-                            z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
-        } else {
-          reinterpret_cast<uint2*>(z.win + ((size_t)u * c.W + (t % c.W)) * kD)[lane] = raw;
-        }
-      }
-      continue;
-    }
+    if ((x == 0 && c.kw) || c.vbits == 4) continue;  // prefill_warp_kernel's rows
     const uint4* src = reinterpret_cast<const uint4*>((x ? v : k) + (size_t)u * T * kD) + 2 * r;
     uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
     if (g0 + q < gend) {
@@ -262,6 +246,41 @@ __global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint
   }
 }
 
+// Rows the bulk layout does not handle -- output-aware K pruning (float32 score keys)
+// and the 4-bit payload (NEXT-4) -- one warp per token. A kernel of its own: the warp-per-token
+// compressor is a chain of warp reductions, so its throughput is the number of resident warps
+// (48 per SM here against the bulk kernel's 24). Grid (ceil(T / 64), min(2U, 65535)), 8 warps
+// of 8 tokens each per block.
+constexpr int kWarpTokPerWarp = 8;
+__global__ void __launch_bounds__(256, 6) prefill_warp_kernel(CacheView c, const uint16_t* __restrict__ k,
+                                                             const uint16_t* __restrict__ v, int T) {
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.y; row < 2 * c.U; row += gridDim.y) {
+    const int x = row >= c.U;  // 0 = K, 1 = V
+    if (!((x == 0 && c.kw) || c.vbits == 4)) continue;
+    const int u = row - x * c.U;
+    const int nc = c.n_comp[u], nw = c.n_win[u], ntok = nc + nw;
+    const int g0 = ((int)blockIdx.x * 8 + (int)(threadIdx.x >> 5)) * kWarpTokPerWarp;
+    if (g0 >= ntok) continue;
+    const int gend = min(g0 + kWarpTokPerWarp, ntok);
+    const Sel z = sel_tensor(c, x);
+    const float* kw = (x == 0 && c.kw) ? c.kw + (size_t)u * kD : nullptr;
+    const uint16_t* base = (x ? v : k) + (size_t)u * T * kD;
+    uint2 nxt = reinterpret_cast<const uint2*>(base + (size_t)g0 * kD)[lane];
+    for (int t = g0; t < gend; ++t) {
+      const uint2 raw = nxt;
+      if (t + 1 < gend) nxt = reinterpret_cast<const uint2*>(base + (size_t)(t + 1) * kD)[lane];  // next token in flight
+      if (t < nc) {
+        const size_t rec = (size_t)u * c.cap + t;
+        compress_raw_warp(raw, z.keep, z.kpad, (uint32_t)t, z.bm + rec * kTiles, z.rec_val(rec),
+                          z.off + rec * kTiles, lane, kw, c.vbits, z.rq);
+      } else {
+        reinterpret_cast<uint2*>(z.win + ((size_t)u * c.W + (t % c.W)) * kD)[lane] = raw;
+      }
+    }
+  }
+}
+
 // Append (decode) mode: block = 2 warps (K, V) per unit.
 __global__ void __launch_bounds__(64) append_kernel(CacheView c, const uint16_t* __restrict__ k_new,
                                                     const uint16_t* __restrict__ v_new) {
@@ -318,7 +337,11 @@ cudaError_t launch_prefill(const CacheView& c, const uint16_t* k, const uint16_t
   if (T == 0 || c.U == 0) return cudaSuccess;
   const int per_block = 8 * 4 * kPrefillGroups;
   const dim3 grid((unsigned)((T + per_block - 1) / per_block), (unsigned)min(2 * c.U, 65535));
-  prefill_kernel<<<grid, 256, 0, s>>>(c, k, v, T);
+  if (c.vbits != 4) prefill_kernel<<<grid, 256, 0, s>>>(c, k, v, T);  // (4-bit: every row is a warp-per-token row)
+  if (c.vbits == 4 || c.kw) {  // the rows of the warp-per-token layout
+    const dim3 gw((unsigned)((T + 8 * kWarpTokPerWarp - 1) / (8 * kWarpTokPerWarp)), (unsigned)min(2 * c.U, 65535));
+    prefill_warp_kernel<<<gw, 256, 0, s>>>(c, k, v, T);
+  }
   return cudaGetLastError();
 }
 

@@ -25,11 +25,11 @@ def algorithmic_bytes(U, T, W, keep, d=128):
     return rd + wr
 
 
-def run(Bt=16, hq=32, hkv=8, T=4096, keep=39, reps=10, W=32):
+def run(Bt=16, hq=32, hkv=8, T=4096, keep=39, reps=10, W=32, vbits=16):
     U = Bt * hkv
     K = synth.fp16_torch((U, T, 128), 11)
     V = synth.fp16_torch((U, T, 128), 12)
-    caches = [M.MustafarCache(Bt, hq, hkv, 128, keep, keep, W, T + 8) for _ in range(2)]
+    caches = [M.MustafarCache(Bt, hq, hkv, 128, keep, keep, W, T + 8, value_bits=vbits) for _ in range(2)]
     for c in caches:
         c.prune_compress_kv(K, V)
     torch.cuda.synchronize()
@@ -41,7 +41,7 @@ def run(Bt=16, hq=32, hkv=8, T=4096, keep=39, reps=10, W=32):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
     nb = algorithmic_bytes(U, T, W, keep)
-    print(f"prefill U={U} T={T} keep={keep}: {us:.1f} us/call, {nb / 1e6:.1f} MB, {nb / us / 1e3:.0f} GB/s",
+    print(f"prefill U={U} T={T} keep={keep} vbits={vbits}: {us:.1f} us/call, {nb / 1e6:.1f} MB, {nb / us / 1e3:.0f} GB/s",
           flush=True)
     return us, nb
 
