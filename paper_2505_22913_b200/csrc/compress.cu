@@ -43,6 +43,9 @@ __global__ void set_counters_uniform(int32_t* n_comp, int32_t* n_win, int U, int
 #define MSTF_PREFILL_GROUPS 8
 #endif
 constexpr int kPrefillGroups = MSTF_PREFILL_GROUPS;  // 4-token groups per warp
+#ifndef MSTF_PREFILL_MINB
+#define MSTF_PREFILL_MINB 4  // resident CTAs per SM (62 registers; 3 CTAs: 76 registers, 2 % slower)
+#endif
 #ifndef MSTF_PREFILL_HSET
 #define MSTF_PREFILL_HSET 1
 #endif
@@ -51,7 +54,7 @@ __device__ __forceinline__ uint32_t __half2_as_u32(__half2 x) { return *reinterp
 __device__ __forceinline__ uint32_t shfl_down8(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d, 8); }
 __device__ __forceinline__ uint32_t shfl_up8(uint32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d, 8); }
 
-__global__ void __launch_bounds__(256, 3) prefill_kernel(CacheView c, const uint16_t* __restrict__ k,
+__global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheView c, const uint16_t* __restrict__ k,
                                                       const uint16_t* __restrict__ v, int T) {
   const int lane = threadIdx.x & 31, q = lane >> 3, r = lane & 7;
   // byte_perm selectors: put byte 3 (resp. 2) of a word into byte q, zeros elsewhere; take byte q
