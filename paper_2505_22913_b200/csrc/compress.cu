@@ -227,11 +227,19 @@ __global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheVi
       // order and [k, kpad) zero padding, R7), then written with 16-byte stores
       uint16_t* sr = s_rec[threadIdx.x >> 5][q];
       {
-        uint32_t p = pos;
+        // a shared-memory byte address advanced per kept value: one predicated store and one
+        // predicated add per value
+        uint32_t a = smem_u32(sr) + 2u * pos;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          if ((m16 >> (2 * i)) & 1u) sr[p++] = (uint16_t)(w[i] & 0xFFFFu);
-          if ((m16 >> (2 * i + 1)) & 1u) sr[p++] = (uint16_t)(w[i] >> 16);
+          if ((m16 >> (2 * i)) & 1u) {
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)(w[i] & 0xFFFFu)) : "memory");
+            a += 2u;
+          }
+          if ((m16 >> (2 * i + 1)) & 1u) {
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)(w[i] >> 16)) : "memory");
+            a += 2u;
+          }
         }
         if (r == 7)
           for (int j = (int)kk; j < z.kpad; ++j) sr[j] = 0;
