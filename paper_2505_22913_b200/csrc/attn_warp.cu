@@ -49,6 +49,12 @@ namespace {
 #ifndef MSTF_B128
 #define MSTF_B128 1  // pair arrays written with 16-byte stores (dev A/B: 0 = 4-byte stores)
 #endif
+#ifndef MSTF_PREFIX
+#define MSTF_PREFIX MSTF_B128  // per-word pair-entry addresses stored by the build lanes (needs MSTF_B128)
+#endif
+#if MSTF_PREFIX && !MSTF_B128
+#error "MSTF_PREFIX stores the prefix addresses in the pad words of the 16-byte-store row layout"
+#endif
 constexpr int kWNst = 2;          // TMA ring depth per warp (blocks in flight)
 constexpr int kWMaxWarps = 16;    // warps per CTA (one CTA per SM, <= 128 registers per thread)
 constexpr int kWHdrInts = 16;
@@ -62,6 +68,7 @@ struct WParams {
   float scale_log2;
   float lazy_log2;        // softmax reference-max slack (log2 units; 0: exact running max)
   int np;                 // workers (warps of the grid)
+  int skew_d;             // worker weights within full CTAs (worker_begin; 0: equal shares)
   int wpc;                // warps per CTA
   int cs, cw;             // cost model: per-segment start, per window block
   int uniform;            // every unit has the same counters (closed-form partition)
@@ -196,8 +203,23 @@ __device__ __forceinline__ uint32_t gather1(uint32_t base, uint32_t cnt, uint32_
 struct TokGather {
   uint32_t x[4], y[4], B[4];
 };
-__device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t base, uint32_t sx) {
+// MSTF_PREFIX: B[1..3] were stored by the token's build lane after its last pair entry (word kp
+// of the row, see build_prefix); the lane loads them instead of three popc + add (XU pipe).
+__device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t base, uint32_t sx, uint32_t kp4) {
   const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#if MSTF_PREFIX
+  const uint4 e = lds128(base + kp4);
+  tg.B[0] = base;
+  tg.B[1] = e.y;
+  tg.B[2] = e.z;
+  tg.B[3] = e.w;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    tg.x[q] = ww[q] << sx;
+    tg.y[q] = ww[q] << (sx - 1);
+  }
+#else
+  (void)kp4;
   uint32_t b = base;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -206,6 +228,20 @@ __device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t 
     tg.B[q] = opaque(b);
     b += 4u * __popc(ww[q]);
   }
+#endif
+}
+// The last pair entry Y[kp] of a token's row and, with MSTF_PREFIX, the addresses of pair entries
+// e_1..e_3 (kept channels before bitmap words 1..3) in the three words after it: one 16-byte
+// store. bm = the token's bitmap words (zero for a token past the block's end: every address is
+// then the row base, inside the region).
+__device__ __forceinline__ void build_tail(uint32_t ydst, int nch, uint32_t last, const uint4 bm) {
+#if MSTF_PREFIX
+  const uint32_t e1 = __popc(bm.x), e2 = e1 + __popc(bm.y), e3 = e2 + __popc(bm.z);
+  sts128(ydst + 32u * nch, last, ydst + 4u * e1, ydst + 4u * e2, ydst + 4u * e3);
+#else
+  (void)bm;
+  sts32(ydst + 32u * nch, last);
+#endif
 }
 // K (score A operand): gather slot j = 2s + hh of lane t is pair 8s + 4hh + t, i.e. channels
 // 16s + 8hh + 2t, +1 -- the natural m16n8k16 k order. Word q = j >> 2, byte m = j & 3; the
@@ -230,7 +266,7 @@ __device__ __forceinline__ uint32_t gather_v(const TokGather& tg) {
 // one prmt each; four entries per 16-byte store. With sw = kp + 4 (4 mod 8 words) the 8 lanes of
 // every quarter-warp store phase hit 8 distinct 16-byte bank groups. raw = this lane's record.
 template <int NCH>
-__device__ __forceinline__ void build_token(uint32_t raw, uint32_t ydst, int nch_rt) {
+__device__ __forceinline__ void build_token(uint32_t raw, uint32_t ydst, int nch_rt, const uint4 bm) {
   const int nch = NCH ? NCH : nch_rt;
   uint32_t prev = 0;
 #pragma unroll
@@ -253,7 +289,7 @@ __device__ __forceinline__ void build_token(uint32_t raw, uint32_t ydst, int nch
 #endif
     prev = a.w;
   }
-  sts32(ydst + 32u * nch, prmt(prev, 0u, 0x5432));
+  build_tail(ydst, nch, prmt(prev, 0u, 0x5432), bm);
 }
 
 // The same pair arrays from a 4-bit record: [scale f16][zero f16][codes,
@@ -296,7 +332,7 @@ __device__ __forceinline__ void q4_word_pairs(uint32_t w, uint32_t sc2, uint32_t
   prev = R[3];
 }
 template <int NCH>
-__device__ __forceinline__ void build_token_q4(uint32_t rec, uint32_t ydst, int nch_rt) {
+__device__ __forceinline__ void build_token_q4(uint32_t rec, uint32_t ydst, int nch_rt, const uint4 bm) {
   uint32_t prev = 0;
   if constexpr (NCH > 0) {
     // the whole record in 16-byte loads (records are 16-byte aligned; scalar loads of 32-byte
@@ -311,12 +347,12 @@ __device__ __forceinline__ void build_token_q4(uint32_t rec, uint32_t ydst, int 
     const uint32_t sc2 = prmt(wv[0], 0u, 0x1010), z2 = prmt(wv[0], 0u, 0x3232);
 #pragma unroll
     for (int c = 0; c < NCH; ++c) q4_word_pairs(wv[1 + c], sc2, z2, ydst + 32u * c, prev);
-    sts32(ydst + 32u * NCH, prmt(prev, 0u, 0x5432));
+    build_tail(ydst, NCH, prmt(prev, 0u, 0x5432), bm);
   } else {
     const uint32_t sz = lds32(rec);
     const uint32_t sc2 = prmt(sz, 0u, 0x1010), z2 = prmt(sz, 0u, 0x3232);
     for (int c = 0; c < nch_rt; ++c) q4_word_pairs(lds32(rec + 4 + 4 * c), sc2, z2, ydst + 32u * c, prev);
-    sts32(ydst + 32u * nch_rt, prmt(prev, 0u, 0x5432));
+    build_tail(ydst, nch_rt, prmt(prev, 0u, 0x5432), bm);
   }
 }
 
@@ -356,7 +392,30 @@ __device__ __forceinline__ int unit_of_cost(const WParams& p, int x, int cpu) {
   }
   return lo;
 }
-__device__ __forceinline__ int worker_begin(long long S, int np, int P) { return (int)((long long)P * S / np); }
+// Worker weights within a full CTA (16 warps, skew d > 0): warp w gets 1000 + d (2 (w >> 2) - 3) per 16000
+// of the CTA's share. The four warps of one SM sub-partition (w, w + 4, w + 8, w + 12) do not run at
+// the same speed under the warp scheduler: with equal shares the trace (tools/trace_attn.py) shows
+// warps 0-3 finishing ~2 % after warps 12-15 at C4 and C2. CTA boundaries are those of equal
+// weights, so the inverse below is a closed form plus a scan of one CTA.
+__device__ __forceinline__ int skew_prefix(int d, int w) {  // sum of the weights of warps 0..w-1
+  const int G = w >> 2, r = w & 3;
+  return 1000 * w + d * (4 * G * (G - 1) - 12 * G + r * (2 * G - 3));
+}
+__device__ __forceinline__ int worker_begin(const WParams& p, long long S, int P) {
+  if (p.skew_d) {
+    const int c = P >> 4, w = P & 15;
+    return (int)(S * (c * 16000LL + skew_prefix(p.skew_d, w)) / ((long long)(p.np >> 4) * 16000LL));
+  }
+  return (int)((long long)P * S / p.np);
+}
+// the worker owning cost unit x: the largest P with worker_begin(P) <= x
+__device__ __forceinline__ int worker_of(const WParams& p, long long S, int x) {
+  if (!p.skew_d) return (int)(((long long)(x + 1) * p.np - 1) / S);
+  const int c = (int)(((long long)(x + 1) * (p.np >> 4) - 1) / S);
+  int w = 15;
+  while (w > 0 && worker_begin(p, S, c * 16 + w) > x) --w;
+  return c * 16 + w;
+}
 
 // Fused step: wait until the unit's append is published (bounded spin: a broken invariant
 // becomes a launch error, not a hung GPU).
@@ -411,12 +470,14 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     p.hdr[0] = (int)S;
     p.hdr[1] = cpu;
   }
-  const int x0 = worker_begin(S, p.np, P), x1 = worker_begin(S, p.np, P + 1);
+  const int x0 = worker_begin(p, S, P), x1 = worker_begin(p, S, P + 1);
 
   // ---- a4 (fused step): tensor x (0: K, 1: V) of unit u is appended by the owner of the unit's
   // start cost unit min(x, cs - 1) -- with cs >= 2 two workers when the partition splits them
   // (small problems: two otherwise idle warps), one worker doing both otherwise
-  if (p.fuse) {
+  // (run after this warp's first TMA issues, so that their latency overlaps the compression)
+  auto fused_appends = [&]() {
+    if (!p.fuse) return;
     for (int u = max(0, x0 / cpu - 1); u < c.U && u * cpu < x1; ++u) {
       for (int x = 0; x < 2; ++x) {
         const int j = u * cpu + min(x, p.cs - 1);
@@ -427,9 +488,11 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
         if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.ready + u), "r"(1) : "memory");
       }
     }
+  };
+  if (x0 >= x1) {  // no cost unit: no append either
+    if (lane == 0) trace_at(P, 1);
+    if (!p.cta_merge) return;
   }
-  if (lane == 0) trace_at(P, 1);
-  if (x0 >= x1 && !p.cta_merge) return;
   if (x0 < x1) {  // (cta_merge: every warp reaches the CTA merge at the end)
 
   // ---- block streams: producer (TMA issue, one block ahead) and consumer walk the same
@@ -499,7 +562,16 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     if (pu >= c.U || unit_start(p, pu, cpu) >= x1) { pdone = true; break; }
     p_unit();
   }
-  for (int k = 0; k < kWNst && !pdone; ++k) {
+  // first stages: issued before this warp's fused appends, except a block that holds a record
+  // this step's append writes (its appender may be this warp)
+  while (pseq < kWNst && !pdone && pb != pwait) {
+    if (lane == 0) p_issue();
+    ++pseq;
+    p_advance();
+  }
+  fused_appends();
+  if (lane == 0) trace_at(P, 1);
+  while (pseq < kWNst && !pdone) {
     if (lane == 0) p_issue();
     ++pseq;
     p_advance();
@@ -521,6 +593,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
                                      : (uint32_t)(p.off_vval + (lane & 15) * p.rqv);
   const uint32_t ydst = lane < 16 ? ypk + 4u * (uint32_t)((lane & 15) * p.swk) : ypv + 4u * (uint32_t)((lane & 15) * p.swv);
   const int nch_me = (lane < 16 ? p.kpk : p.kpv) >> 3;
+  const uint32_t bm_off = lane < 16 ? (uint32_t)(16 * (lane & 15)) : (uint32_t)(p.off_vbm + 16 * (lane & 15));
   int qu = -1;
   int cseq = 0;  // compressed blocks consumed
 
@@ -650,10 +723,12 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       mbar_wait_u32(bar0 + 8 * s, (uint32_t)(cseq / kWNst) & 1u);
       if (cseq == 0 && lane == 0) trace_at(P, 2);
       const int nvalid = min(16, cn.nc - b * 16);
+      // this lane's token's bitmap words (for the pair-entry prefix addresses)
+      const uint4 bm_me = MSTF_PREFIX && (lane & 15) < nvalid ? lds128(st + bm_off) : make_uint4(0u, 0u, 0u, 0u);
       if constexpr (Q4)
-        build_token_q4<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
+        build_token_q4<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me, bm_me);
       else
-        build_token<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me);
+        build_token<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me, bm_me);
       // bitmaps (4 words) of K tokens g, g + 8 and V tokens 2t, 2t+1, 8+2t, 9+2t (R5, R6)
       const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
       const uint4 kb0 = g < nvalid ? lds128(st + 16 * g) : z4;
@@ -677,8 +752,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       float sc[4];
       {
         TokGather t0, t1;
-        tok_prep(t0, kb0, ypk + 4u * (uint32_t)(g * p.swk), 7u - 2u * (uint32_t)t);
-        tok_prep(t1, kb1, ypk + 4u * (uint32_t)((g + 8) * p.swk), 7u - 2u * (uint32_t)t);
+        tok_prep(t0, kb0, ypk + 4u * (uint32_t)(g * p.swk), 7u - 2u * (uint32_t)t, 4u * (uint32_t)p.kpk);
+        tok_prep(t1, kb1, ypk + 4u * (uint32_t)((g + 8) * p.swk), 7u - 2u * (uint32_t)t, 4u * (uint32_t)p.kpk);
         float s2[4] = {0.f, 0.f, 0.f, 0.f};
         sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
 #define MSTF_KS(S)                                                                                              \
@@ -693,8 +768,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       auto vgather = [&](int ks, uint32_t (&va)[8], uint32_t (&vb)[8]) {
         TokGather ta, tb;
         const uint32_t sx = 15u - 2u * (uint32_t)g;
-        tok_prep(ta, vbm[2 * ks], ypv + 4u * (uint32_t)(tk[2 * ks] * p.swv), sx);
-        tok_prep(tb, vbm[2 * ks + 1], ypv + 4u * (uint32_t)(tk[2 * ks + 1] * p.swv), sx);
+        tok_prep(ta, vbm[2 * ks], ypv + 4u * (uint32_t)(tk[2 * ks] * p.swv), sx, 4u * (uint32_t)p.kpv);
+        tok_prep(tb, vbm[2 * ks + 1], ypv + 4u * (uint32_t)(tk[2 * ks + 1] * p.swv), sx, 4u * (uint32_t)p.kpv);
         va[0] = gather_v<0, 0>(ta); va[4] = gather_v<0, 1>(ta); vb[0] = gather_v<0, 0>(tb); vb[4] = gather_v<0, 1>(tb);
         va[1] = gather_v<1, 0>(ta); va[5] = gather_v<1, 1>(ta); vb[1] = gather_v<1, 0>(tb); vb[5] = gather_v<1, 1>(tb);
         va[2] = gather_v<2, 0>(ta); va[6] = gather_v<2, 1>(ta); vb[2] = gather_v<2, 0>(tb); vb[6] = gather_v<2, 1>(tb);
@@ -825,7 +900,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     // merge the CTA's warp partials per unit (shared memory) into one partial (slot CTA + u of ws2)
     __syncthreads();
     const int cb = (int)blockIdx.x, wpc = p.wpc;
-    const int X0 = worker_begin(S, p.np, cb * wpc), X1 = worker_begin(S, p.np, (cb + 1) * wpc);
+    const int X0 = worker_begin(p, S, cb * wpc), X1 = worker_begin(p, S, (cb + 1) * wpc);
     if (X0 < X1) {
       const int uA = unit_of_cost(p, X0, cpu), uB = unit_of_cost(p, X1 - 1, cpu);
       const uint32_t wb = (uint32_t)p.warp_bytes / 4;
@@ -913,18 +988,35 @@ __global__ void mstf_cost_prefix_kernel(const WParams p) {
 // In a fused step it then writes the unit's post-append counters and clears its ready flag.
 template <bool SUB>
 __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p) {
-  pdl_launch_dependents();
-  pdl_wait();  // partials and the plan header come from the attention kernel just before
-  if (threadIdx.x == 0) trace_at(65536 + blockIdx.x, 0);
   extern __shared__ __align__(16) float s_comb[];
   const int G = p.G;
   const int u = blockIdx.x, wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = SUB ? wi % G : wi, sub = SUB ? wi / G : 0, Sn = SUB ? blockDim.x / (32 * G) : 1;
-  const long long S = p.hdr[0];
-  const int cpu = p.hdr[1];
+  // Uniform caches: the partition (S, cost per unit) follows from this unit's own counters, which
+  // only this CTA writes (below) and which were last written one decode step ago -- read before
+  // the grid-dependency wait, so that the wait is followed directly by the partial loads. This
+  // kernel signals its dependents only after its wait: a running combine then implies that
+  // every kernel before the attention launch it follows has completed (R-PDL, DESIGN 7.1).
+  int nc_u = 0, nw_u = 0, cpu = 0;
+  long long S = 0;
+  if (p.uniform) {
+    nc_u = p.c.n_comp[u];
+    nw_u = p.c.n_win[u];
+    int nc = nc_u;
+    if (p.fuse && (p.c.W == 0 || nw_u == p.c.W)) nc += 1;  // counters_of, from the values just read
+    cpu = cost_of(p, nc);
+    S = (long long)p.c.U * cpu;
+  }
+  pdl_wait();  // partials (and the ragged cost prefix) come from the kernels just before
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) trace_at(65536 + blockIdx.x, 0);
+  if (!p.uniform) {
+    S = p.hdr[0];
+    cpu = p.hdr[1];
+  }
   const int us = cpu ? u * cpu : p.pref[u], ue = cpu ? (u + 1) * cpu : p.pref[u + 1];
   // workers overlapping [us, ue): first = owner of us, last = owner of ue - 1
-  int wf = (int)(((long long)(us + 1) * p.np - 1) / S), wl = (int)(((long long)ue * p.np - 1) / S);
+  int wf = worker_of(p, S, us), wl = worker_of(p, S, ue - 1);
   const float* ws_o = p.ws_o;
   const float* ws_ml = p.ws_ml;
   if (p.cta_merge) {  // one partial per CTA (slot CTA + u of ws2)
@@ -1011,7 +1103,7 @@ __global__ void __launch_bounds__(512) mstf_warp_combine_kernel(const WParams p)
   }
   if (threadIdx.x == 0) trace_at(65536 + blockIdx.x, 1);
   if (p.fuse && threadIdx.x == 0) {  // a4 bookkeeping of the fused step (after every reader)
-    const int nc = p.c.n_comp[u], nw = p.c.n_win[u];
+    const int nc = nc_u, nw = nw_u;  // (fuse implies uniform caches: read before the wait)
     if (p.c.W == 0 || nw == p.c.W) p.c.n_comp[u] = nc + 1; else p.c.n_win[u] = nw + 1;
     p.ready[u] = 0;
   }
@@ -1124,6 +1216,9 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   // running max when the caller receives the partials themselves (m = max, the ABI contract)
   p.lazy_log2 = part_ml ? 0.f : 8.f;
   p.np = plan.grid * plan.wpc;
+  // dev A/B knob (read once): the skew of the worker weights (0: equal shares)
+  static const int s_skew = std::getenv("MSTF_SKEW") ? std::atoi(std::getenv("MSTF_SKEW")) : 0;
+  p.skew_d = plan.wpc == 16 && !plan.cta_merge ? std::max(0, std::min(s_skew, 50)) : 0;
   p.wpc = plan.wpc;
   sk_cost_params(&p.cs, &p.cw);
   p.uniform = uniform;

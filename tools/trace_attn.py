@@ -42,6 +42,15 @@ res = {"B": B, "T": T, "fused": fused, "workers": int(act.sum()),
        "done_us": [round(float(rel[:, 3][w[:, 3] > 0].min()), 2), round(float(rel[:, 3][w[:, 3] > 0].median()), 2), round(float(rel[:, 3][w[:, 3] > 0].max()), 2)],
        "combine_start_us": [round(float(((comb[:, 0] - t0) / 1e3).min()), 2), round(float(((comb[:, 0] - t0) / 1e3).max()), 2)] if len(comb) else None,
        "combine_done_us": [round(float(((comb[:, 1] - t0) / 1e3).min()), 2), round(float(((comb[:, 1] - t0) / 1e3).max()), 2)] if len(comb) else None}
+# appenders (fused step): workers whose append phase took > 0.5 us
+app = (rel[:, 1] - rel[:, 0]) > 0.5
+if bool(app.any()):
+    res["appenders"] = int(app.sum())
+    res["appender_done_us"] = [round(float(rel[app, 3].median()), 2), round(float(rel[app, 3].max()), 2)]
+    res["appender_first_block_us"] = [round(float(rel[app, 2].median()), 2), round(float(rel[app, 2].max()), 2)]
+    res["other_done_us"] = [round(float(rel[~app, 3].median()), 2), round(float(rel[~app, 3].max()), 2)]
+print(json.dumps(res), flush=True)
+res = {}
 # per-CTA spread (workers = CTA * wpc + warp; wpc from the number of active workers / 148 if full)
 wpc = int(sys.argv[4]) if len(sys.argv) > 4 else 16
 d = (tr[:65536, 3].double() - t0) / 1e3
