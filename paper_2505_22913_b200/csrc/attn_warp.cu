@@ -68,7 +68,6 @@ struct WParams {
   float scale_log2;
   float lazy_log2;        // softmax reference-max slack (log2 units; 0: exact running max)
   int np;                 // workers (warps of the grid)
-  int skew_d;             // worker weights within full CTAs (worker_begin; 0: equal shares)
   int wpc;                // warps per CTA
   int cs, cw;             // cost model: per-segment start, per window block
   int uniform;            // every unit has the same counters (closed-form partition)
@@ -392,29 +391,10 @@ __device__ __forceinline__ int unit_of_cost(const WParams& p, int x, int cpu) {
   }
   return lo;
 }
-// Worker weights within a full CTA (16 warps, skew d > 0): warp w gets 1000 + d (2 (w >> 2) - 3) per 16000
-// of the CTA's share. The four warps of one SM sub-partition (w, w + 4, w + 8, w + 12) do not run at
-// the same speed under the warp scheduler: with equal shares the trace (tools/trace_attn.py) shows
-// warps 0-3 finishing ~2 % after warps 12-15 at C4 and C2. CTA boundaries are those of equal
-// weights, so the inverse below is a closed form plus a scan of one CTA.
-__device__ __forceinline__ int skew_prefix(int d, int w) {  // sum of the weights of warps 0..w-1
-  const int G = w >> 2, r = w & 3;
-  return 1000 * w + d * (4 * G * (G - 1) - 12 * G + r * (2 * G - 3));
-}
-__device__ __forceinline__ int worker_begin(const WParams& p, long long S, int P) {
-  if (p.skew_d) {
-    const int c = P >> 4, w = P & 15;
-    return (int)(S * (c * 16000LL + skew_prefix(p.skew_d, w)) / ((long long)(p.np >> 4) * 16000LL));
-  }
-  return (int)((long long)P * S / p.np);
-}
+__device__ __forceinline__ int worker_begin(const WParams& p, long long S, int P) { return (int)((long long)P * S / p.np); }
 // the worker owning cost unit x: the largest P with worker_begin(P) <= x
 __device__ __forceinline__ int worker_of(const WParams& p, long long S, int x) {
-  if (!p.skew_d) return (int)(((long long)(x + 1) * p.np - 1) / S);
-  const int c = (int)(((long long)(x + 1) * (p.np >> 4) - 1) / S);
-  int w = 15;
-  while (w > 0 && worker_begin(p, S, c * 16 + w) > x) --w;
-  return c * 16 + w;
+  return (int)(((long long)(x + 1) * p.np - 1) / S);
 }
 
 // Fused step: wait until the unit's append is published (bounded spin: a broken invariant
@@ -1216,9 +1196,6 @@ cudaError_t launch_warp_attention(const CacheView& c, const WarpPlan& plan, int3
   // running max when the caller receives the partials themselves (m = max, the ABI contract)
   p.lazy_log2 = part_ml ? 0.f : 8.f;
   p.np = plan.grid * plan.wpc;
-  // dev A/B knob (read once): the skew of the worker weights (0: equal shares)
-  static const int s_skew = std::getenv("MSTF_SKEW") ? std::atoi(std::getenv("MSTF_SKEW")) : 0;
-  p.skew_d = plan.wpc == 16 && !plan.cta_merge ? std::max(0, std::min(s_skew, 50)) : 0;
   p.wpc = plan.wpc;
   sk_cost_params(&p.cs, &p.cw);
   p.uniform = uniform;

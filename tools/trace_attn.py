@@ -43,7 +43,8 @@ res = {"B": B, "T": T, "fused": fused, "workers": int(act.sum()),
        "combine_start_us": [round(float(((comb[:, 0] - t0) / 1e3).min()), 2), round(float(((comb[:, 0] - t0) / 1e3).max()), 2)] if len(comb) else None,
        "combine_done_us": [round(float(((comb[:, 1] - t0) / 1e3).min()), 2), round(float(((comb[:, 1] - t0) / 1e3).max()), 2)] if len(comb) else None}
 # appenders (fused step): workers whose append phase took > 0.5 us
-app = (rel[:, 1] - rel[:, 0]) > 0.5
+ph = rel[:, 1] - rel[:, 0]
+app = ph > float(ph.median()) + 1.0
 if bool(app.any()):
     res["appenders"] = int(app.sum())
     res["appender_done_us"] = [round(float(rel[app, 3].median()), 2), round(float(rel[app, 3].max()), 2)]
