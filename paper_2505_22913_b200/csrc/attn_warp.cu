@@ -52,6 +52,9 @@ namespace {
 #ifndef MSTF_PREFIX
 #define MSTF_PREFIX MSTF_B128  // per-word pair-entry addresses stored by the build lanes (needs MSTF_B128)
 #endif
+#ifndef MSTF_PREFIX_SEL
+#define MSTF_PREFIX_SEL 3  // which token preps load the stored addresses: bit 0 = K, bit 1 = V (dev A/B)
+#endif
 #if MSTF_PREFIX && !MSTF_B128
 #error "MSTF_PREFIX stores the prefix addresses in the pad words of the 16-byte-store row layout"
 #endif
@@ -204,9 +207,21 @@ struct TokGather {
 };
 // MSTF_PREFIX: B[1..3] were stored by the token's build lane after its last pair entry (word kp
 // of the row, see build_prefix); the lane loads them instead of three popc + add (XU pipe).
+template <bool LOAD>
 __device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t base, uint32_t sx, uint32_t kp4) {
   const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #if MSTF_PREFIX
+  if (!LOAD) {
+    uint32_t b = base;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      tg.x[q] = ww[q] << sx;
+      tg.y[q] = ww[q] << (sx - 1);
+      tg.B[q] = opaque(b);
+      b += 4u * __popc(ww[q]);
+    }
+    return;
+  }
   const uint4 e = lds128(base + kp4);
   tg.B[0] = base;
   tg.B[1] = e.y;
@@ -732,8 +747,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       float sc[4];
       {
         TokGather t0, t1;
-        tok_prep(t0, kb0, ypk + 4u * (uint32_t)(g * p.swk), 7u - 2u * (uint32_t)t, 4u * (uint32_t)p.kpk);
-        tok_prep(t1, kb1, ypk + 4u * (uint32_t)((g + 8) * p.swk), 7u - 2u * (uint32_t)t, 4u * (uint32_t)p.kpk);
+        tok_prep<(MSTF_PREFIX_SEL & 1) != 0>(t0, kb0, ypk + 4u * (uint32_t)(g * p.swk), 7u - 2u * (uint32_t)t, 4u * (uint32_t)p.kpk);
+        tok_prep<(MSTF_PREFIX_SEL & 1) != 0>(t1, kb1, ypk + 4u * (uint32_t)((g + 8) * p.swk), 7u - 2u * (uint32_t)t, 4u * (uint32_t)p.kpk);
         float s2[4] = {0.f, 0.f, 0.f, 0.f};
         sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
 #define MSTF_KS(S)                                                                                              \
@@ -748,8 +763,8 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       auto vgather = [&](int ks, uint32_t (&va)[8], uint32_t (&vb)[8]) {
         TokGather ta, tb;
         const uint32_t sx = 15u - 2u * (uint32_t)g;
-        tok_prep(ta, vbm[2 * ks], ypv + 4u * (uint32_t)(tk[2 * ks] * p.swv), sx, 4u * (uint32_t)p.kpv);
-        tok_prep(tb, vbm[2 * ks + 1], ypv + 4u * (uint32_t)(tk[2 * ks + 1] * p.swv), sx, 4u * (uint32_t)p.kpv);
+        tok_prep<(MSTF_PREFIX_SEL & 2) != 0>(ta, vbm[2 * ks], ypv + 4u * (uint32_t)(tk[2 * ks] * p.swv), sx, 4u * (uint32_t)p.kpv);
+        tok_prep<(MSTF_PREFIX_SEL & 2) != 0>(tb, vbm[2 * ks + 1], ypv + 4u * (uint32_t)(tk[2 * ks + 1] * p.swv), sx, 4u * (uint32_t)p.kpv);
         va[0] = gather_v<0, 0>(ta); va[4] = gather_v<0, 1>(ta); vb[0] = gather_v<0, 0>(tb); vb[4] = gather_v<0, 1>(tb);
         va[1] = gather_v<1, 0>(ta); va[5] = gather_v<1, 1>(ta); vb[1] = gather_v<1, 0>(tb); vb[5] = gather_v<1, 1>(tb);
         va[2] = gather_v<2, 0>(ta); va[6] = gather_v<2, 1>(ta); vb[2] = gather_v<2, 0>(tb); vb[6] = gather_v<2, 1>(tb);
