@@ -495,10 +495,11 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   const int u_first = unit_of_cost(p, x0, cpu);
   // producer cursor: unit pu, next block pb, end pbe; pnc = pu's compressed tokens (as the
   // attention sees them), pwait = the block holding the record the fused append writes (-1: none);
-  // g_* = global addresses of block pb's four runs (K bitmaps, K values, V bitmaps, V values),
-  // advanced by one block per issue
+  // prec = record index of block pb's first token (u * cap + 16 pb: < 2^32, a cache of 2^32
+  // records would not fit in HBM); the four runs' global addresses (K bitmaps, K values, V bitmaps,
+  // V values) are formed from it at issue time (one wide multiply-add each)
   int pu = u_first, pb = 0, pbe = 0, pseq = 0, pnc = 0, pwait = -1;
-  const uint8_t *g_kbm = nullptr, *g_kv = nullptr, *g_vbm = nullptr, *g_vv = nullptr;
+  uint32_t prec = 0;
   bool pdone = false;
   auto seg_bounds = [&](int u, int& lo, int& hi, int& nbc, Counters& cn) {
     cn = counters_of(p, u);
@@ -516,20 +517,13 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     pnc = cn.nc;
     // fused step with an eviction: record cn.nc - 1 is written by the unit's appender
     pwait = (p.fuse && (c.W == 0 || cn.nw == c.W) && cn.nc > 0) ? (cn.nc - 1) / 16 : -1;
-    const size_t rec = (size_t)pu * c.cap + (size_t)pb * 16;
-    g_kbm = reinterpret_cast<const uint8_t*>(c.bm[0]) + rec * 16;
-    g_vbm = reinterpret_cast<const uint8_t*>(c.bm[1]) + rec * 16;
-    g_kv = reinterpret_cast<const uint8_t*>(c.val[0]) + rec * p.rqk;
-    g_vv = reinterpret_cast<const uint8_t*>(c.val[1]) + rec * p.rqv;
+    prec = (uint32_t)pu * (uint32_t)c.cap + 16u * (uint32_t)pb;
   };
   p_unit();
   // advance the producer to its next compressed block (or done)
   auto p_advance = [&]() {
     ++pb;
-    g_kbm += 256;
-    g_vbm += 256;
-    g_kv += 16 * p.rqk;
-    g_vv += 16 * p.rqv;
+    prec += 16u;
     while (!pdone && pb >= pbe) {
       ++pu;
       if (pu >= c.U || unit_start(p, pu, cpu) >= x1) { pdone = true; break; }
@@ -546,6 +540,10 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     const int s = pseq & (kWNst - 1);
     const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes), bar = bar0 + 8 * s;
     const uint32_t bytes_bm = n * 16, bytes_k = n * p.rqk, bytes_v = n * p.rqv;
+    const uint8_t* g_kbm = reinterpret_cast<const uint8_t*>(c.bm[0]) + (size_t)prec * 16u;
+    const uint8_t* g_vbm = reinterpret_cast<const uint8_t*>(c.bm[1]) + (size_t)prec * 16u;
+    const uint8_t* g_kv = reinterpret_cast<const uint8_t*>(c.val[0]) + (size_t)prec * (uint32_t)p.rqk;
+    const uint8_t* g_vv = reinterpret_cast<const uint8_t*>(c.val[1]) + (size_t)prec * (uint32_t)p.rqv;
     mbar_expect_tx_u32(bar, 2 * bytes_bm + bytes_k + bytes_v);
     bulk_g2s_u32(st, g_kbm, bytes_bm, bar);
     bulk_g2s_u32(st + p.off_kval, g_kv, bytes_k, bar);
