@@ -52,6 +52,9 @@ namespace {
 #ifndef MSTF_PREFIX
 #define MSTF_PREFIX MSTF_B128  // per-word pair-entry addresses stored by the build lanes (needs MSTF_B128)
 #endif
+#ifndef MSTF_UNIFORM
+#define MSTF_UNIFORM 1  // per-warp scalars made provably warp-uniform (dev A/B: 0)
+#endif
 #ifndef MSTF_PREFIX_SEL
 #define MSTF_PREFIX_SEL 3  // which token preps load the stored addresses: bit 0 = K, bit 1 = V (dev A/B)
 #endif
@@ -179,6 +182,14 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 // Global data published by another CTA (generic stores + release / acquire) must be visible to
 // a TMA read issued after the acquire.
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// elect.sync over the full warp: true on exactly one lane (the lowest, lane 0 here)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void l2_prefetch(const void* ptr, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
@@ -433,9 +444,16 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const CacheView& c = p.c;
+#if MSTF_UNIFORM
+  // The warp index (hence every per-warp scalar) through a shuffle from lane 0: ptxas then knows
+  // these values are warp-uniform and keeps the TMA operands in uniform registers (no
+  // elect / R2UR broadcast loop around each cp.async.bulk).
+  const int P = __shfl_sync(0xffffffffu, (int)blockIdx.x * p.wpc + warp, 0);
+#else
   const int P = (int)blockIdx.x * p.wpc + warp;
+#endif
   // per-warp region: [stages kWNst x stage_bytes][pairs K 16 x swk words][pairs V][mbarriers]
-  const uint32_t wbase = smem_u32(smem) + (uint32_t)(warp * p.warp_bytes);
+  const uint32_t wbase = smem_u32(smem) + (uint32_t)((P - (int)blockIdx.x * p.wpc) * p.warp_bytes);
   const uint32_t ypk = wbase + (uint32_t)(kWNst * p.stage_bytes);  // 128-byte aligned
   const uint32_t ypv = ypk + ((64u * (uint32_t)p.swk + 127u) & ~127u) + (MSTF_B128 ? 0u : 4u);
   const uint32_t bar0 = (max(ypv + 64u * (uint32_t)p.swv, ypk + (uint32_t)kWPartBytes) + 7u) & ~7u;
@@ -518,6 +536,14 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
     // fused step with an eviction: record cn.nc - 1 is written by the unit's appender
     pwait = (p.fuse && (c.W == 0 || cn.nw == c.W) && cn.nc > 0) ? (cn.nc - 1) / 16 : -1;
     prec = (uint32_t)pu * (uint32_t)c.cap + 16u * (uint32_t)pb;
+#if MSTF_UNIFORM
+    // (the counters come from global loads: re-assert warp-uniformity of the cursor)
+    pb = __shfl_sync(0xffffffffu, pb, 0);
+    pbe = __shfl_sync(0xffffffffu, pbe, 0);
+    pnc = __shfl_sync(0xffffffffu, pnc, 0);
+    pwait = __shfl_sync(0xffffffffu, pwait, 0);
+    prec = __shfl_sync(0xffffffffu, prec, 0);
+#endif
   };
   p_unit();
   // advance the producer to its next compressed block (or done)
@@ -530,25 +556,43 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       p_unit();
     }
   };
-  auto p_issue = [&]() {  // lane 0: TMA of block (pu, pb) into stage pseq % kWNst
-    const uint32_t n = (uint32_t)min(16, pnc - pb * 16);
+  // lane 0: TMA of block (pu, pb) into stage pseq % kWNst; pr = its record index, ns = 2 n + stage
+  // (passed in so that they can be made provably warp-uniform before the lane-0 branch)
+  auto p_issue = [&](uint32_t pr, uint32_t ns) {
+    const uint32_t n = ns >> 1;
     if (pb == pwait) {
       // this block holds the record the step's append writes: wait for it (TMA = async proxy)
       wait_ready(p.ready + pu);
       fence_proxy_async_global();
     }
-    const int s = pseq & (kWNst - 1);
-    const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes), bar = bar0 + 8 * s;
+    const uint32_t s = ns & 1u;
+    const uint32_t st = wbase + s * (uint32_t)p.stage_bytes, bar = bar0 + 8u * s;
     const uint32_t bytes_bm = n * 16, bytes_k = n * p.rqk, bytes_v = n * p.rqv;
-    const uint8_t* g_kbm = reinterpret_cast<const uint8_t*>(c.bm[0]) + (size_t)prec * 16u;
-    const uint8_t* g_vbm = reinterpret_cast<const uint8_t*>(c.bm[1]) + (size_t)prec * 16u;
-    const uint8_t* g_kv = reinterpret_cast<const uint8_t*>(c.val[0]) + (size_t)prec * (uint32_t)p.rqk;
-    const uint8_t* g_vv = reinterpret_cast<const uint8_t*>(c.val[1]) + (size_t)prec * (uint32_t)p.rqv;
+    const uint8_t* g_kbm = reinterpret_cast<const uint8_t*>(c.bm[0]) + (size_t)pr * 16u;
+    const uint8_t* g_vbm = reinterpret_cast<const uint8_t*>(c.bm[1]) + (size_t)pr * 16u;
+    const uint8_t* g_kv = reinterpret_cast<const uint8_t*>(c.val[0]) + (size_t)pr * (uint32_t)p.rqk;
+    const uint8_t* g_vv = reinterpret_cast<const uint8_t*>(c.val[1]) + (size_t)pr * (uint32_t)p.rqv;
     mbar_expect_tx_u32(bar, 2 * bytes_bm + bytes_k + bytes_v);
     bulk_g2s_u32(st, g_kbm, bytes_bm, bar);
     bulk_g2s_u32(st + p.off_kval, g_kv, bytes_k, bar);
     bulk_g2s_u32(st + p.off_vbm, g_vbm, bytes_bm, bar);
     bulk_g2s_u32(st + p.off_vval, g_vv, bytes_v, bar);
+  };
+  // every lane: the issue of the next block (fence: the stage is being refilled, WAR vs the TMA)
+  auto p_issue_warp = [&](bool fence) {
+    uint32_t pr = prec, ns = 2u * (uint32_t)min(16, pnc - pb * 16) + (uint32_t)(pseq & (kWNst - 1));
+#if MSTF_UNIFORM
+    pr = __shfl_sync(0xffffffffu, pr, 0);
+    ns = __shfl_sync(0xffffffffu, ns, 0);
+#endif
+#if MSTF_UNIFORM
+    if (elect_one()) {  // (lane 0; an elected lane lets ptxas drop the per-copy uniformity loop)
+#else
+    if (lane == 0) {
+#endif
+      if (fence) fence_proxy_async_smem();
+      p_issue(pr, ns);
+    }
   };
   while (!pdone && pb >= pbe) {  // first unit may hold no compressed block of this range
     ++pu;
@@ -558,14 +602,14 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   // first stages: issued before this warp's fused appends, except a block that holds a record
   // this step's append writes (its appender may be this warp)
   while (pseq < kWNst && !pdone && pb != pwait) {
-    if (lane == 0) p_issue();
+    p_issue_warp(false);
     ++pseq;
     p_advance();
   }
   fused_appends();
   if (lane == 0) trace_at(P, 1);
   while (pseq < kWNst && !pdone) {
-    if (lane == 0) p_issue();
+    p_issue_warp(false);
     ++pseq;
     p_advance();
   }
@@ -733,10 +777,7 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       __syncwarp();
       // the stage is fully read: refill it with block cseq + kWNst (WAR vs the TMA write)
       if (!pdone) {
-        if (lane == 0) {
-          fence_proxy_async_smem();
-          p_issue();
-        }
+        p_issue_warp(true);
         ++pseq;
         p_advance();
       }
