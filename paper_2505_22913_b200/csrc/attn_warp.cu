@@ -55,6 +55,9 @@ namespace {
 #ifndef MSTF_UNIFORM
 #define MSTF_UNIFORM 1  // per-warp scalars made provably warp-uniform (dev A/B: 0)
 #endif
+#ifndef MSTF_ZBM
+#define MSTF_ZBM 1  // bitmap slots past a partial block's end zeroed in the stage (dev A/B: 0 = predicated loads)
+#endif
 #ifndef MSTF_PREFIX_SEL
 #define MSTF_PREFIX_SEL 3  // which token preps load the stored addresses: bit 0 = K, bit 1 = V (dev A/B)
 #endif
@@ -761,19 +764,35 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       if (cseq == 0 && lane == 0) trace_at(P, 2);
       const int nvalid = min(16, cn.nc - b * 16);
       // this lane's token's bitmap words (for the pair-entry prefix addresses)
-      const uint4 bm_me = MSTF_PREFIX && (lane & 15) < nvalid ? lds128(st + bm_off) : make_uint4(0u, 0u, 0u, 0u);
+      const bool tok_ok = (lane & 15) < nvalid;
+      const uint4 bm_me = MSTF_PREFIX && tok_ok ? lds128(st + bm_off) : make_uint4(0u, 0u, 0u, 0u);
+#if MSTF_ZBM
+      // a token past the block's end (partial last block): its bitmap slot in the stage holds
+      // stale bytes; the token's lane zeroes it, so that every lane below loads bitmaps
+      // unconditionally (zero bits: masked gathers, prefix addresses at the row base)
+      if (!tok_ok) sts128(st + bm_off, 0u, 0u, 0u, 0u);
+#endif
       if constexpr (Q4)
         build_token_q4<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me, bm_me);
       else
         build_token<NK == NV ? NK : 0>(st + raw_off, ydst, nch_me, bm_me);
       // bitmaps (4 words) of K tokens g, g + 8 and V tokens 2t, 2t+1, 8+2t, 9+2t (R5, R6)
+      const int tk[4] = {2 * t, 2 * t + 1, 8 + 2 * t, 9 + 2 * t};
+#if MSTF_ZBM
+      __syncwarp();  // the zeroed slots before the other lanes' loads
+      const uint4 kb0 = lds128(st + 16 * g);
+      const uint4 kb1 = lds128(st + 16 * (g + 8));
+      uint4 vbm[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) vbm[x] = lds128(st + p.off_vbm + 16 * tk[x]);
+#else
       const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
       const uint4 kb0 = g < nvalid ? lds128(st + 16 * g) : z4;
       const uint4 kb1 = g + 8 < nvalid ? lds128(st + 16 * (g + 8)) : z4;
-      const int tk[4] = {2 * t, 2 * t + 1, 8 + 2 * t, 9 + 2 * t};
       uint4 vbm[4];
 #pragma unroll
       for (int x = 0; x < 4; ++x) vbm[x] = tk[x] < nvalid ? lds128(st + p.off_vbm + 16 * tk[x]) : z4;
+#endif
       __syncwarp();
       // the stage is fully read: refill it with block cseq + kWNst (WAR vs the TMA write)
       if (!pdone) {
