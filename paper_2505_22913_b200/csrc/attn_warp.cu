@@ -58,6 +58,9 @@ namespace {
 #ifndef MSTF_ZBM
 #define MSTF_ZBM 1  // bitmap slots past a partial block's end zeroed in the stage (dev A/B: 0 = predicated loads)
 #endif
+#ifndef MSTF_PREFIX_PACK
+#define MSTF_PREFIX_PACK 0  // 1: the three prefix counts packed in one word (dev A/B; slower, DESIGN 8.1)
+#endif
 #ifndef MSTF_PREFIX_SEL
 #define MSTF_PREFIX_SEL 3  // which token preps load the stored addresses: bit 0 = K, bit 1 = V (dev A/B)
 #endif
@@ -236,7 +239,17 @@ __device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t 
     }
     return;
   }
+#if MSTF_PREFIX_PACK
+  // e_1..e_3 packed in bytes 0..2 of the word after Y[kp]: one 4-byte load (one wavefront for the
+  // tokens of a gather instruction) instead of a shared 16-byte load (one per quarter-warp)
+  const uint32_t pk = lds32(base + kp4 + 4u);
+  uint4 e;
+  e.y = base + 4u * (pk & 0xFFu);
+  e.z = base + 4u * ((pk >> 8) & 0xFFu);
+  e.w = base + 4u * (pk >> 16);
+#else
   const uint4 e = lds128(base + kp4);
+#endif
   tg.B[0] = base;
   tg.B[1] = e.y;
   tg.B[2] = e.z;
@@ -265,7 +278,11 @@ __device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t 
 __device__ __forceinline__ void build_tail(uint32_t ydst, int nch, uint32_t last, const uint4 bm) {
 #if MSTF_PREFIX
   const uint32_t e1 = __popc(bm.x), e2 = e1 + __popc(bm.y), e3 = e2 + __popc(bm.z);
+#if MSTF_PREFIX_PACK
+  sts128(ydst + 32u * nch, last, e1 | (e2 << 8) | (e3 << 16), 0u, 0u);
+#else
   sts128(ydst + 32u * nch, last, ydst + 4u * e1, ydst + 4u * e2, ydst + 4u * e3);
+#endif
 #else
   (void)bm;
   sts32(ydst + 32u * nch, last);

@@ -53,7 +53,14 @@ __device__ __forceinline__ __half2 __ushort2_as_half2(uint32_t x) { return *rein
 __device__ __forceinline__ uint32_t __half2_as_u32(__half2 x) { return *reinterpret_cast<uint32_t*>(&x); }
 __device__ __forceinline__ uint32_t shfl_down8(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d, 8); }
 __device__ __forceinline__ uint32_t shfl_up8(uint32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d, 8); }
+__device__ __forceinline__ uint32_t shfl_xor8(uint32_t v, int d) { return __shfl_xor_sync(0xffffffffu, v, d, 8); }
+// Rows of tensor x that the bulk layout cannot handle: output-aware K (float32 score keys) and
+// 4-bit records with more than 8 code words (k > 64: more words than the token's eight lanes).
+__device__ __forceinline__ bool warp_row(const CacheView& c, int x) {
+  return (x == 0 && c.kw) || (c.vbits == 4 && (x ? c.keep[1] : c.keep[0]) > 64);
+}
 
+template <bool Q4>  // the 4-bit payload (c.vbits == 4): its own instantiation, so the fp16 one carries no extra code
 __global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheView c, const uint16_t* __restrict__ k,
                                                       const uint16_t* __restrict__ v, int T) {
   const int lane = threadIdx.x & 31, q = lane >> 3, r = lane & 7;
@@ -64,6 +71,7 @@ __global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheVi
   // per warp and token slot: the packed record; rows of kD + 8 halves (66 words: the four token
   // slots of a warp start in different banks, so their 2-byte stores do not conflict)
   __shared__ __align__(16) uint16_t s_rec[8][4][kD + 8];
+  __shared__ __align__(16) uint32_t s_q4[Q4 ? 8 : 1][4][16];  // 4-bit payload: the token's record words
   for (int row = blockIdx.y; row < 2 * c.U; row += gridDim.y) {
     const int x = row >= c.U;  // 0 = K, 1 = V
     const int u = row - x * c.U;
@@ -73,7 +81,7 @@ __global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheVi
     const Sel z = sel_tensor(c, x);
     const uint32_t kk = (uint32_t)z.keep;
     const int gend = min(g0 + 4 * kPrefillGroups, ntok);
-    if ((x == 0 && c.kw) || c.vbits == 4) continue;  // prefill_warp_kernel's rows
+    if (warp_row(c, x)) continue;  // prefill_warp_kernel's rows
     const uint4* src = reinterpret_cast<const uint4*>((x ? v : k) + (size_t)u * T * kD) + 2 * r;
     uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
     if (g0 + q < gend) {
@@ -245,12 +253,66 @@ __global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheVi
           for (int j = (int)kk; j < z.kpad; ++j) sr[j] = 0;
       }
       __syncwarp();
+      // NEXT-4 (R25-R27): the kept values (slots [0, k) of the staged record, in
+      // channel order) -> per-token fp16 scale / zero point and 4-bit codes, the arithmetic of
+      // quantize_token_warp: zero = min, scale = f16((max - min) / 15) (1 if 0 or not finite),
+      // code = rint(clamp((x - zero) * (1 / scale), 0, 15)). Lane r owns code word r (slots
+      // 8r..8r+7, k <= 64); min / max over the token's eight lanes by three shuffles of the
+      // packed pair (min key, 0xFFFF - max key).
+      constexpr bool q4 = Q4;
+      if constexpr (q4) {
+        const int ncw = ((int)kk + 7) >> 3;
+        uint4 v8 = make_uint4(0u, 0u, 0u, 0u);
+        if (r < ncw) v8 = reinterpret_cast<const uint4*>(sr)[r];
+        const uint32_t hv[4] = {v8.x, v8.y, v8.z, v8.w};
+        uint32_t kmn = 0xFFFFu, kmx = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t h = (hv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+          if (8 * r + j < (int)kk) {
+            const uint32_t key = f16_order_key(h);
+            kmn = min(kmn, key);
+            kmx = max(kmx, key);
+          }
+        }
+        uint32_t pk = (kmn << 16) | (0xFFFFu - kmx);
+#pragma unroll
+        for (int d = 1; d < 8; d <<= 1) pk = __vminu2(pk, shfl_xor8(pk, d));
+        const uint32_t zero_bits = f16_from_key(pk >> 16), max_bits = f16_from_key(0xFFFFu - (pk & 0xFFFFu));
+        const float lo = __half2float(__ushort_as_half((unsigned short)zero_bits));
+        const float hi = __half2float(__ushort_as_half((unsigned short)max_bits));
+        __half sc = __float2half_rn(__fdiv_rn(__fsub_rn(hi, lo), 15.f));
+        const float scf = __half2float(sc);
+        if (!(scf != 0.f && isfinite(scf))) sc = __float2half_rn(1.f);
+        const float inv = __frcp_rn(__half2float(sc));
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t h = (hv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+          if (8 * r + j < (int)kk) {
+            const float xv = __half2float(__ushort_as_half((unsigned short)h));
+            const float rr = fminf(fmaxf(__fmul_rn(__fsub_rn(xv, lo), inv), 0.f), 15.f);
+            word |= (uint32_t)rintf(rr) << (4 * j);
+          }
+        }
+        // record words: [0] scale | zero << 16, [1 + r] code word r, zeros up to rq / 4
+        uint32_t* sq = s_q4[threadIdx.x >> 5][q];
+        if (r < ncw) sq[1 + r] = word;
+        if (r == 0) sq[0] = (uint32_t)__half_as_ushort(sc) | (zero_bits << 16);
+        if (ncw + 1 + r < z.rq / 4) sq[ncw + 1 + r] = 0u;
+        __syncwarp();
+      }
       if (valid && t < nc) {
         const size_t rec = (size_t)u * c.cap + t;
         if ((r & 1) == 0) reinterpret_cast<uint32_t*>(z.bm + rec * kTiles)[r >> 1] = m16 | (hi16 << 16);
         if ((r & 3) == 0) z.off[rec * kTiles + (r >> 2)] = (uint32_t)t * (uint32_t)z.kpad + pos;
-        uint4* vo = reinterpret_cast<uint4*>(z.val + rec * z.kpad);
-        for (int j = r; j < z.kpad / 8; j += 8) vo[j] = reinterpret_cast<const uint4*>(sr)[j];
+        if constexpr (q4) {
+          if (r < z.rq / 16)
+            reinterpret_cast<uint4*>(z.rec_val(rec))[r] = reinterpret_cast<const uint4*>(s_q4[threadIdx.x >> 5][q])[r];
+        } else {
+          uint4* vo = reinterpret_cast<uint4*>(z.val + rec * z.kpad);
+          for (int j = r; j < z.kpad / 8; j += 8) vo[j] = reinterpret_cast<const uint4*>(sr)[j];
+        }
       }
       __syncwarp();  // the stage is rewritten by the next group
     }
@@ -258,7 +320,7 @@ __global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheVi
 }
 
 // Rows the bulk layout does not handle -- output-aware K pruning (float32 score keys)
-// and the 4-bit payload (NEXT-4) -- one warp per token. A kernel of its own: the warp-per-token
+// and 4-bit records of more than 64 kept values (NEXT-4) -- one warp per token. A kernel of its own: the warp-per-token
 // compressor is a chain of warp reductions, so its throughput is the number of resident warps
 // (48 per SM here against the bulk kernel's 24). Grid (ceil(T / 64), min(2U, 65535)), 8 warps
 // of 8 tokens each per block.
@@ -268,7 +330,7 @@ __global__ void __launch_bounds__(256, 6) prefill_warp_kernel(CacheView c, const
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.y; row < 2 * c.U; row += gridDim.y) {
     const int x = row >= c.U;  // 0 = K, 1 = V
-    if (!((x == 0 && c.kw) || c.vbits == 4)) continue;
+    if (!warp_row(c, x)) continue;
     const int u = row - x * c.U;
     const int nc = c.n_comp[u], nw = c.n_win[u], ntok = nc + nw;
     const int g0 = ((int)blockIdx.x * 8 + (int)(threadIdx.x >> 5)) * kWarpTokPerWarp;
@@ -348,8 +410,15 @@ cudaError_t launch_prefill(const CacheView& c, const uint16_t* k, const uint16_t
   if (T == 0 || c.U == 0) return cudaSuccess;
   const int per_block = 8 * 4 * kPrefillGroups;
   const dim3 grid((unsigned)((T + per_block - 1) / per_block), (unsigned)min(2 * c.U, 65535));
-  if (c.vbits != 4) prefill_kernel<<<grid, 256, 0, s>>>(c, k, v, T);  // (4-bit: every row is a warp-per-token row)
-  if (c.vbits == 4 || c.kw) {  // the rows of the warp-per-token layout
+  const bool wk = c.kw != nullptr || (c.vbits == 4 && (c.keep[0] > 64 || c.keep[1] > 64));
+  const bool bulk = !(c.kw != nullptr && c.vbits == 4 && c.keep[1] > 64);  // some row is a bulk row
+  if (bulk) {
+    if (c.vbits == 4)
+      prefill_kernel<true><<<grid, 256, 0, s>>>(c, k, v, T);
+    else
+      prefill_kernel<false><<<grid, 256, 0, s>>>(c, k, v, T);
+  }
+  if (wk) {  // the rows of the warp-per-token layout
     const dim3 gw((unsigned)((T + 8 * kWarpTokPerWarp - 1) / (8 * kWarpTokPerWarp)), (unsigned)min(2 * c.U, 65535));
     prefill_warp_kernel<<<gw, 256, 0, s>>>(c, k, v, T);
   }
