@@ -58,6 +58,9 @@ namespace {
 #ifndef MSTF_ZBM
 #define MSTF_ZBM 1  // bitmap slots past a partial block's end zeroed in the stage (dev A/B: 0 = predicated loads)
 #endif
+#ifndef MSTF_BOUNDS
+#define MSTF_BOUNDS 0
+#endif
 #ifndef MSTF_PREFIX_PACK
 #define MSTF_PREFIX_PACK 0  // 1: the three prefix counts packed in one word (dev A/B; slower, DESIGN 8.1)
 #endif
@@ -221,12 +224,26 @@ __device__ __forceinline__ uint32_t gather1(uint32_t base, uint32_t cnt, uint32_
 // immediate k that drops the bits above it, so Y[e_q + that] is the pair (R8, R6).
 struct TokGather {
   uint32_t x[4], y[4], B[4];
+#if MSTF_BOUNDS
+  uint32_t lo, hi;  // the token's pair entries Y[0..kp]: [lo, hi]
+#endif
 };
+// MSTF_BOUNDS (dev build, -DMSTF_BOUNDS=1): every data-dependent shared-memory address of the
+// expansion -- the stored prefix addresses and each gather -- is checked against its token's
+// pair-entry range; a violation traps (the GPU parity tests then fail). Used in place of
+// compute-sanitizer, which this GPU pool does not allow.
+__device__ __forceinline__ void bounds_check(uint32_t a, uint32_t lo, uint32_t hi) {
+  if (a < lo || a > hi) __trap();
+}
 // MSTF_PREFIX: B[1..3] were stored by the token's build lane after its last pair entry (word kp
 // of the row, see build_prefix); the lane loads them instead of three popc + add (XU pipe).
 template <bool LOAD>
 __device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t base, uint32_t sx, uint32_t kp4) {
   const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#if MSTF_BOUNDS
+  tg.lo = base;
+  tg.hi = base + kp4;
+#endif
 #if MSTF_PREFIX
   if (!LOAD) {
     uint32_t b = base;
@@ -249,6 +266,11 @@ __device__ __forceinline__ void tok_prep(TokGather& tg, const uint4 w, uint32_t 
   e.w = base + 4u * (pk >> 16);
 #else
   const uint4 e = lds128(base + kp4);
+#endif
+#if MSTF_BOUNDS
+  bounds_check(e.y, tg.lo, tg.hi);
+  bounds_check(e.z, tg.lo, tg.hi);
+  bounds_check(e.w, tg.lo, tg.hi);
 #endif
   tg.B[0] = base;
   tg.B[1] = e.y;
@@ -295,6 +317,9 @@ template <int J>
 __device__ __forceinline__ uint32_t gather_k(const TokGather& tg) {
   constexpr int q = J >> 2, m = J & 3;
   const uint32_t cnt = __popc(m == 3 ? tg.x[q] : tg.x[q] << (24 - 8 * m));
+#if MSTF_BOUNDS
+  bounds_check(tg.B[q] + 4u * cnt, tg.lo, tg.hi);
+#endif
   return gather1(tg.B[q], cnt, pair_mask<m>(tg.x[q], tg.y[q]));
 }
 // V (value A operand): row r (0: g, 1: g + 8) of m-tile mt is pair 16mt + 8r + g, i.e. word mt,
@@ -302,6 +327,9 @@ __device__ __forceinline__ uint32_t gather_k(const TokGather& tg) {
 template <int MT, int R>
 __device__ __forceinline__ uint32_t gather_v(const TokGather& tg) {
   const uint32_t cnt = __popc(R ? tg.x[MT] : tg.x[MT] << 16);
+#if MSTF_BOUNDS
+  bounds_check(tg.B[MT] + 4u * cnt, tg.lo, tg.hi);
+#endif
   return gather1(tg.B[MT], cnt, pair_mask<1 + 2 * R>(tg.x[MT], tg.y[MT]));
 }
 

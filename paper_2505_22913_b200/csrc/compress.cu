@@ -46,6 +46,9 @@ constexpr int kPrefillGroups = MSTF_PREFILL_GROUPS;  // 4-token groups per warp
 #ifndef MSTF_PREFILL_MINB
 #define MSTF_PREFILL_MINB 4  // resident CTAs per SM (62 registers; 3 CTAs: 76 registers, 2 % slower)
 #endif
+#ifndef MSTF_BOUNDS
+#define MSTF_BOUNDS 0  // dev build: device-side bounds / invariant checks that trap (no compute-sanitizer here)
+#endif
 #ifndef MSTF_PREFILL_HSET
 #define MSTF_PREFILL_HSET 1
 #endif
@@ -251,6 +254,12 @@ __global__ void __launch_bounds__(256, MSTF_PREFILL_MINB) prefill_kernel(CacheVi
         }
         if (r == 7)
           for (int j = (int)kk; j < z.kpad; ++j) sr[j] = 0;
+#if MSTF_BOUNDS
+        // dev build: the staged values stay inside the token's k slots, and the token keeps
+        // exactly k channels (a2)
+        if (valid && a > smem_u32(sr) + 2u * kk) __trap();
+        if (valid && r == 7 && pos + pc != kk) __trap();
+#endif
       }
       __syncwarp();
       // NEXT-4 (R25-R27): the kept values (slots [0, k) of the staged record, in
