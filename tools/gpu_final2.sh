@@ -22,8 +22,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:mstf
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:prefill_kernel -s 2 -c 1 \
    -o gpurun_out/prof_prefill python tools/prefill_time.py 16 32 8 4096 39 > gpurun_out/ncu_pf.log 2>&1
-T="tests/test_gpu_parity.py::test_attention_matches_oracle tests/test_gpu_parity.py::test_decode_step_equals_append_then_attention tests/test_gpu_quant.py"
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 --log-file gpurun_out/san_memcheck.log python -m pytest $T -q -p no:cacheprovider > gpurun_out/san_memcheck_pytest.log 2>&1
-echo "rc=$?" >> gpurun_out/san_memcheck_pytest.log
-timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 --log-file gpurun_out/san_racecheck.log python -m pytest $T -q -p no:cacheprovider > gpurun_out/san_racecheck_pytest.log 2>&1
-echo "rc=$?" >> gpurun_out/san_racecheck_pytest.log
+# (compute-sanitizer is closed on this pool: see tools/gpu_bounds.sh for the device-side checks)
