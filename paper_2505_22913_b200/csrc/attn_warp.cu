@@ -7,7 +7,11 @@
 //   * its compressed blocks are streamed from HBM by TMA bulk copies (cp.async.bulk, four per
 //     block: K bitmaps, K values, V bitmaps, V values -- each a contiguous run of fixed-stride
 //     records, R5-R7) into a private 2-stage shared-memory ring; the warp issues them itself
-//     two blocks ahead, so the hot loop has no global-load instruction;
+//     two blocks ahead, so the hot loop has no global-load instruction; the copies' operands
+//     are made provably warp-uniform (shuffled from lane 0, issued by an elect.sync lane), so
+//     ptxas keeps them in uniform registers (MSTF_UNIFORM);
+//   * the token's build lane also stores the pair-entry addresses of bitmap words 1-3 (prefix
+//     counts) in its row's pad words, which the consumer lanes load (MSTF_PREFIX);
 //   * expansion ("load as compressed, compute as dense"): one lane per token rewrites
 //     the packed values as a shifted pair array Y[m] = (h[m-1], h[m]); channel pair (2j, 2j+1)
 //     of a bitmap word with exclusive prefix e is then ONE aligned 32-bit load
