@@ -419,8 +419,9 @@ cudaError_t launch_prefill(const CacheView& c, const uint16_t* k, const uint16_t
   if (T == 0 || c.U == 0) return cudaSuccess;
   const int per_block = 8 * 4 * kPrefillGroups;
   const dim3 grid((unsigned)((T + per_block - 1) / per_block), (unsigned)min(2 * c.U, 65535));
-  const bool wk = c.kw != nullptr || (c.vbits == 4 && (c.keep[0] > 64 || c.keep[1] > 64));
-  const bool bulk = !(c.kw != nullptr && c.vbits == 4 && c.keep[1] > 64);  // some row is a bulk row
+  // (host mirror of warp_row: which tensors' rows each kernel handles)
+  const bool wr0 = c.kw != nullptr || (c.vbits == 4 && c.keep[0] > 64), wr1 = c.vbits == 4 && c.keep[1] > 64;
+  const bool wk = wr0 || wr1, bulk = !(wr0 && wr1);
   if (bulk) {
     if (c.vbits == 4)
       prefill_kernel<true><<<grid, 256, 0, s>>>(c, k, v, T);
