@@ -75,6 +75,12 @@ namespace {
 #error "MSTF_PREFIX stores the prefix addresses in the pad words of the 16-byte-store row layout"
 #endif
 constexpr int kWNst = 2;          // TMA ring depth per warp (blocks in flight)
+#ifndef MSTF_PREISSUE
+#define MSTF_PREISSUE 1
+#endif
+// stages issued before the first block is consumed (the rest once the first block has landed:
+// the first blocks of all workers then share the HBM fill alone; dev A/B)
+constexpr int kPreIssue = MSTF_PREISSUE < kWNst ? MSTF_PREISSUE : kWNst;
 constexpr int kWMaxWarps = 16;    // warps per CTA (one CTA per SM, <= 128 registers per thread)
 constexpr int kWHdrInts = 16;
 constexpr int kWPartBytes = 4 * 128 * 4 + 4 * 2 * 4;  // a warp's partial in shared memory (G <= 4)
@@ -653,14 +659,14 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
   }
   // first stages: issued before this warp's fused appends, except a block that holds a record
   // this step's append writes (its appender may be this warp)
-  while (pseq < kWNst && !pdone && pb != pwait) {
+  while (pseq < kPreIssue && !pdone && pb != pwait) {
     p_issue_warp(false);
     ++pseq;
     p_advance();
   }
   fused_appends();
   if (lane == 0) trace_at(P, 1);
-  while (pseq < kWNst && !pdone) {
+  while (pseq < kPreIssue && !pdone) {
     p_issue_warp(false);
     ++pseq;
     p_advance();
@@ -811,6 +817,13 @@ __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mst
       const uint32_t st = wbase + (uint32_t)(s * p.stage_bytes);
       mbar_wait_u32(bar0 + 8 * s, (uint32_t)(cseq / kWNst) & 1u);
       if (cseq == 0 && lane == 0) trace_at(P, 2);
+      if constexpr (kPreIssue < kWNst) {  // top the ring up once the first block has landed
+        if (!pdone && pseq < cseq + kWNst) {
+          p_issue_warp(false);  // (into the other stage: never used yet)
+          ++pseq;
+          p_advance();
+        }
+      }
       const int nvalid = min(16, cn.nc - b * 16);
       // this lane's token's bitmap words (for the pair-entry prefix addresses)
       const bool tok_ok = (lane & 15) < nvalid;
