@@ -79,8 +79,9 @@ constexpr int kWNst = 2;          // TMA ring depth per warp (blocks in flight)
 #define MSTF_PREISSUE 1
 #endif
 // stages issued before the first block is consumed (the rest once the first block has landed:
-// the first blocks of all workers then share the HBM fill alone; dev A/B)
-constexpr int kPreIssue = MSTF_PREISSUE < kWNst ? MSTF_PREISSUE : kWNst;
+// the first blocks of all workers then share the HBM fill alone; fp16 payload only -- the 4-bit
+// payload measured faster with both stages at entry, C4_q4 531.8 vs 541.1 us; dev A/B)
+constexpr int kPreIssueF16 = MSTF_PREISSUE < kWNst ? MSTF_PREISSUE : kWNst;
 constexpr int kWMaxWarps = 16;    // warps per CTA (one CTA per SM, <= 128 registers per thread)
 constexpr int kWHdrInts = 16;
 constexpr int kWPartBytes = 4 * 128 * 4 + 4 * 2 * 4;  // a warp's partial in shared memory (G <= 4)
@@ -499,6 +500,7 @@ __device__ __forceinline__ void wait_ready(const int* flag) {
 template <int NK, int NV, bool G8, bool Q4>
 __global__ void __launch_bounds__(G8 ? kWMaxWarps * 16 : kWMaxWarps * 32, 1) mstf_attn_warp_kernel(const WParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kPreIssue = Q4 ? kWNst : kPreIssueF16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const CacheView& c = p.c;
