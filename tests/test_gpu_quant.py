@@ -73,6 +73,25 @@ def test_q4_prefill_and_appends_bit_exact(M, kind, kk, kv):
     compare(gc, oc, f"append {kind} {kk},{kv}")
 
 
+@pytest.mark.parametrize("W", [0, 5, 32])
+@pytest.mark.parametrize("kk,kv", [(39, 39), (64, 8)])
+def test_q4_bulk_prefill_ragged(M, W, kk, kv):
+    """The 4-bit payload through the bulk prefill kernel (k <= 64: one code word per lane of the
+    token's eight) on ragged units: lengths 0, 1, W, W + 1 and long ones across the kernel's
+    4-token groups and 32-token warp spans; every record buffer bit-exact (R25-R26)."""
+    U_b, hkv, T = 2, 4, 300
+    U = U_b * hkv
+    lengths = [0, 1, W, W + 1, 300, 137, 64, 33]
+    K = synth.fp16_np((U, T, 128), synth.seed_for(90 + W, kk), "normal")
+    V = synth.fp16_np((U, T, 128), synth.seed_for(91 + W, kv), "lattice")
+    gc = M.MustafarCache(U_b, 8, hkv, 128, kk, kv, W, T, value_bits=4)
+    oc = O.OracleCache(U, 128, kk, kv, W, T, value_bits=4)
+    gc.prune_compress_kv(dev(K), dev(V), lengths=lengths)
+    oc.prefill(K.view(np.uint16), V.view(np.uint16), lengths=lengths)
+    torch.cuda.synchronize()
+    compare(gc, oc, f"ragged W={W} {kk},{kv}")
+
+
 @pytest.mark.parametrize("case", [
     # (batch, hq, hkv, T, keep_k, keep_v, W, lengths)
     (1, 1, 1, 64, 64, 64, 32, None),
